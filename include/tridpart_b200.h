@@ -1,0 +1,193 @@
+/*
+ * tridpart_b200.h — C-ABI of the B200-native (sm_100a) partition solver.
+ *
+ * Drop-in boundary for the reference `tridpart` header-only C++20 library
+ * (/root/reference/proj/include/tridpart). The reference has no C ABI of its
+ * own; each entry point below names the reference function whose contract it
+ * replaces (file:line, paths relative to /root/reference/proj/). Plain
+ * pointers and sizes only — no C++ or torch types. The C++ shim
+ * include/tridpart_b200.hpp rebuilds the reference's `tridpart::` API
+ * (same names, same exception types) on top of these calls.
+ *
+ * Conventions
+ *   - System arrays are the reference's SoA layout (tridiagonal.hpp:22-28):
+ *     row i reads sub[i]*x[i-1] + diag[i]*x[i] + super[i]*x[i+1] = rhs[i].
+ *     sub[0] and super[n-1] are never used numerically (as in the reference).
+ *   - `sizes[0..nsizes)` is RecursionPolicy::sizes (partition.hpp:176-187):
+ *     nsizes == 1 is the non-recursive method, nsizes == R+1 recursive depth R.
+ *   - Every call returns a tp_status; on failure `err` (may be NULL) carries
+ *     the code, the zero-pivot row and level, and a message.
+ *   - A tp_ctx owns one CUDA device, a stream, a workspace and CUDA-graph
+ *     caches. It is not thread-safe: use one context per host thread
+ *     (the reference is reentrant, partition.hpp has no shared state).
+ */
+#ifndef TRIDPART_B200_H
+#define TRIDPART_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TP_ABI_VERSION 1
+
+/* Error classes of include/tridpart/errors.hpp:7-96. */
+typedef enum tp_status {
+    TP_OK = 0,
+    TP_ERR_ZERO_PIVOT = 1,          /* ZeroPivotError(row)          errors.hpp:16-24 */
+    TP_ERR_INVALID_SIZE = 2,        /* InvalidSizeError             errors.hpp:26-29 */
+    TP_ERR_DEPTH_OUT_OF_RANGE = 3,  /* DepthOutOfRangeError         errors.hpp:31-34 */
+    TP_ERR_EMPTY_TRAINING_SET = 4,  /* EmptyTrainingSetError        errors.hpp:38-41 */
+    TP_ERR_K_TOO_LARGE = 5,         /* KTooLargeError               errors.hpp:43-46 */
+    TP_ERR_MALFORMED_HEADER = 6,    /* MalformedHeaderError         errors.hpp:70-73 */
+    TP_ERR_BAD_NUMBER = 7,          /* BadNumberError(line)         errors.hpp:75-84 */
+    TP_ERR_IO = 8,                  /* Error("cannot open ...")     io.hpp:80-84     */
+    TP_ERR_CUDA = 9,                /* device / runtime failure (no reference analogue) */
+    TP_ERR_INVALID_ARGUMENT = 10,   /* NULL pointer, bad rank, ... */
+    TP_ERR_NCCL = 11                /* reserved for the collective path */
+} tp_status;
+
+typedef struct tp_error {
+    int32_t code;   /* tp_status */
+    int32_t level;  /* partition level of a zero pivot (0 = the input system) */
+    int64_t row;    /* ZeroPivotError::row() (row index within that level) */
+    char msg[256];
+} tp_error;
+
+typedef struct tp_ctx tp_ctx;
+
+/* ---------------------------------------------------------------- context */
+int32_t tp_abi_version(void);
+tp_status tp_ctx_create(int32_t device, tp_ctx** out, tp_error* err);
+void tp_ctx_destroy(tp_ctx* ctx);
+/* Stream used by the synchronous host-pointer calls (cudaStream_t; NULL = ctx-owned). */
+tp_status tp_ctx_set_stream(tp_ctx* ctx, void* stream, tp_error* err);
+/* Disable/enable CUDA-graph capture of the device solve (default enabled). */
+tp_status tp_ctx_set_graphs(tp_ctx* ctx, int32_t enabled, tp_error* err);
+/* Number of kernels the last solve on this context launched (0 if none). */
+int64_t tp_ctx_last_launch_count(const tp_ctx* ctx);
+
+/* ---------------------------------------------------- the partition solve */
+/* solve_partition(sys, policy) — partition.hpp:244-248 (validation :235-242).
+ * Host pointers, synchronous; x receives n doubles. */
+tp_status tp_solve_partition_f64(tp_ctx* ctx, const double* sub, const double* diag,
+                                 const double* super, const double* rhs, int64_t n,
+                                 const int64_t* sizes, int32_t nsizes, double* x, tp_error* err);
+
+/* Same contract on DEVICE pointers, asynchronous on `stream` (cudaStream_t,
+ * NULL = ctx stream). Zero pivots are detected on the device: call
+ * tp_check_device_error after synchronising the stream. */
+tp_status tp_solve_partition_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                     const double* super, const double* rhs, int64_t n,
+                                     const int64_t* sizes, int32_t nsizes, double* x, void* stream,
+                                     tp_error* err);
+tp_status tp_check_device_error(tp_ctx* ctx, tp_error* err);
+
+/* Observer overload solve_partition(sys, policy, on_interface) — partition.hpp:235-242,
+ * hook at :206. Host pointers; after the solve, `cb` receives each level's
+ * assembled interface system (host copies, valid during the call), level 0 first. */
+typedef void (*tp_interface_cb)(int64_t level, int64_t n, const double* sub, const double* diag,
+                                const double* super, const double* rhs, void* user);
+tp_status tp_solve_partition_observe_f64(tp_ctx* ctx, const double* sub, const double* diag,
+                                         const double* super, const double* rhs, int64_t n,
+                                         const int64_t* sizes, int32_t nsizes, double* x,
+                                         tp_interface_cb cb, void* user, tp_error* err);
+
+/* thomas_solve(sys) — tridiagonal.hpp:52-72. Same solution, computed by the
+ * device finishing solver (exact parallel elimination, not a sequential sweep). */
+tp_status tp_thomas_solve_f64(tp_ctx* ctx, const double* sub, const double* diag,
+                              const double* super, const double* rhs, int64_t n, double* x,
+                              tp_error* err);
+
+/* residual_inf(sys, x) — tridiagonal.hpp:74-87, on device pointers (synchronous). */
+tp_status tp_residual_inf_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                  const double* super, const double* rhs, int64_t n,
+                                  const double* x, double* out, tp_error* err);
+
+/* ------------------------------------------------ sharded (multi-GPU) solve
+ * Contiguous shard [row0, row0+n_local) of a global system, one rank per GPU.
+ * 1) tp_shard_reduce: all local levels + reduction of the shard to its two
+ *    boundary equations, written to eq8_dev as {sub[2], diag[2], super[2], rhs[2]}
+ *    (the assemble_interface rows of partition.hpp:139-149 for the shard).
+ * 2) the caller all-gathers the 8 doubles of every rank (rank order).
+ * 3) tp_shard_finish: solves the 2P-row top system redundantly and expands the
+ *    local levels (Stage 3) into x_dev. Same ctx, pointers and sizes as step 1. */
+tp_status tp_shard_reduce_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                  const double* super, const double* rhs, int64_t n_local,
+                                  const int64_t* sizes, int32_t nsizes, double* eq8_dev,
+                                  void* stream, tp_error* err);
+tp_status tp_shard_finish_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                  const double* super, const double* rhs, int64_t n_local,
+                                  const int64_t* sizes, int32_t nsizes, const double* eq_all_dev,
+                                  int32_t nranks, int32_t rank, double* x_dev, void* stream,
+                                  tp_error* err);
+
+/* --------------------------------------------------- synthetic inputs */
+/* Device analogue of generate_system(n, seed, delta) — bench.hpp:68-93: same
+ * distributions, counter-based (rows [row0, row0+n) of an n_global system),
+ * not bit-identical to std::mt19937_64. */
+tp_status tp_generate_system_f64_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global,
+                                     uint64_t seed, double delta, double* sub, double* diag,
+                                     double* super, double* rhs, void* stream, tp_error* err);
+
+/* ------------------------------------------------------- plan / profile */
+/* make_plan(n, m) — partition.hpp:30-49. bounds (optional) gets K+1 entries. */
+tp_status tp_make_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* nblocks, tp_error* err);
+
+/* Level structure the device solve will execute: per level its size and m;
+ * n_final is the size of the system handed to the finishing solver. */
+tp_status tp_plan_levels(int64_t n, const int64_t* sizes, int32_t nsizes, int64_t* level_n,
+                         int64_t* level_m, int32_t* nlevels, int32_t max_levels, int64_t* n_final,
+                         tp_error* err);
+
+/* Instrumented device solve: per-kernel durations (ms) measured with CUDA
+ * events on the launch stream; names receive "<stage>:L<level>" labels. */
+tp_status tp_solve_profile_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                   const double* super, const double* rhs, int64_t n,
+                                   const int64_t* sizes, int32_t nsizes, double* x,
+                                   float* kernel_ms, char* names /* [max_kernels][32] */,
+                                   int32_t max_kernels, int32_t* nkernels, tp_error* err);
+
+/* ------------------------------------------------------ kNN predictors */
+/* predict(model, n) — knn.hpp:57-77 (feature_of :38): k-NN on log10(N);
+ * distance ties -> smaller N, vote ties -> smaller label. Host code. */
+tp_status tp_predict(const int64_t* pairs_n, const int32_t* pairs_label, int64_t npairs, int32_t k,
+                     int64_t n, int32_t* label, tp_error* err);
+/* fit_knn(train, k) — knn.hpp:40-55: validates k and sorts pairs by n (stable). */
+tp_status tp_fit_knn(int64_t* pairs_n, int32_t* pairs_label, int64_t npairs, int32_t k,
+                     tp_error* err);
+/* recursion_sizes(n, depth, size_model) — policy.hpp:25-45 (kMaxRecursionDepth=4). */
+tp_status tp_recursion_sizes(int64_t n, int32_t depth, const int64_t* pairs_n,
+                             const int32_t* pairs_label, int64_t npairs, int32_t k,
+                             int64_t* sizes /* >= 5 */, int32_t* nsizes, tp_error* err);
+/* The bundled models: which = 0 -> fit_knn(Table I FP64 corrected, k=1),
+ * which = 1 -> fit_depth_model(Table II) (test_policy.cpp:14-21). */
+tp_status tp_default_model(int32_t which, int64_t* pairs_n, int32_t* pairs_label, int64_t cap,
+                           int64_t* npairs, int32_t* k, tp_error* err);
+
+/* read_observations(path) — io.hpp:80-138. Folds rows by (N, precision,
+ * device); the is_opt row carries the label (m, or opt_R for depth rows). */
+typedef struct tp_observation {
+    int64_t n;
+    int32_t label;
+    int32_t corrected;      /* valid when has_corrected */
+    int32_t has_corrected;
+    int32_t depth_label;
+    int32_t streams;
+    int32_t ntimes;
+    char precision[16];
+    char device[48];
+} tp_observation;
+typedef struct tp_obs_set tp_obs_set;
+tp_status tp_obs_read(const char* path, tp_obs_set** out, int64_t* count, tp_error* err);
+tp_status tp_obs_get(const tp_obs_set* set, int64_t i, tp_observation* out, int32_t* cand,
+                     double* times_ms /* ntimes each, may be NULL */, tp_error* err);
+void tp_obs_free(tp_obs_set* set);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRIDPART_B200_H */

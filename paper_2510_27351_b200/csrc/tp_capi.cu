@@ -1,0 +1,888 @@
+// C-ABI layer: context, level planner, CUDA-graph cache and the entry points
+// declared in include/tridpart_b200.h.
+//
+// The planner restates detail::solve_partition_level (partition.hpp:191-224):
+//   level l with n_l < 4            -> finishing solve of that system      (:197)
+//   else make_plan(n_l, sizes[l])   -> Stage 1, interface of 2*K_l rows    (:199-205)
+//   l == depth                      -> finishing solve of the interface    (:208-211)
+//   Stage 3 back up every level                                           (:213-222)
+// The finishing solve runs on the device (single CTA, k_generic<kSolve>); a
+// final system larger than kFinalCap first gets extra device-internal
+// partition levels (m = 32). Those do not change the policy, only how the
+// thomas_solve(iface) of the reference is computed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tridpart_b200.h"
+#include "tp_kernels.h"
+
+using tpb::IfacePtrs;
+using tpb::SysPtrs;
+
+namespace {
+
+constexpr int64_t kInternalM = 32;
+
+void set_err(tp_error* err, tp_status code, const std::string& msg, int64_t row = -1, int32_t level = -1) {
+    if (!err) return;
+    err->code = code;
+    err->row = row;
+    err->level = level;
+    std::snprintf(err->msg, sizeof(err->msg), "%s", msg.c_str());
+}
+void clear_err(tp_error* err) {
+    if (!err) return;
+    err->code = TP_OK;
+    err->row = -1;
+    err->level = -1;
+    err->msg[0] = 0;
+}
+
+#define TP_CUDA(call)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            set_err(err, TP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+            return TP_ERR_CUDA;                                                            \
+        }                                                                                  \
+    } while (0)
+
+// make_plan — partition.hpp:30-49 (block count only).
+int64_t plan_blocks(int64_t n, int64_t m) {
+    if (m >= n) return 1;
+    int64_t leading = n / m;
+    if (n % m <= 1) --leading;
+    return leading + 1;
+}
+
+struct Level {
+    int64_t n = 0;      // rows of this level's system
+    int64_t m = 0;      // requested block size
+    int64_t K = 0;      // blocks (make_plan)
+    int64_t kfull = 0;  // blocks of exactly m rows
+    int64_t tail = 0;   // length of the final block when != m (0 = none)
+    bool internal = false;
+    // bound pointers
+    SysPtrs in{};
+    double* x_out = nullptr;  // solution of this level's system
+    IfacePtrs iface{};        // next level's system (2K rows)
+    double* x_iface = nullptr;
+};
+
+struct Plan {
+    std::vector<Level> levels;
+    int64_t n_final = 0;
+    SysPtrs final_in{};
+    double* final_x = nullptr;
+    size_t ws_doubles = 0;
+};
+
+inline size_t pad32(size_t v) { return (v + 31) & ~size_t(31); }
+
+bool build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan& p) {
+    p.levels.clear();
+    int64_t cur = n;
+    int lvl = 0;
+    size_t ws = 0;
+    while (nsizes > 0) {
+        if (cur < 4) break;
+        Level L;
+        L.n = cur;
+        L.m = sizes[lvl];
+        L.K = plan_blocks(cur, L.m);
+        const int64_t last_len = cur - (L.K - 1) * L.m;
+        if (L.m >= cur) {
+            L.kfull = (cur == L.m) ? 1 : 0;
+            L.tail = (cur == L.m) ? 0 : cur;
+        } else if (last_len == L.m) {
+            L.kfull = L.K;
+            L.tail = 0;
+        } else {
+            L.kfull = L.K - 1;
+            L.tail = last_len;
+        }
+        ws += 5 * pad32((size_t)(2 * L.K));
+        p.levels.push_back(L);
+        cur = 2 * L.K;
+        if (lvl == nsizes - 1) break;
+        ++lvl;
+    }
+    // device-internal levels so the finishing solve fits one CTA
+    while (cur > tpb::kFinalCap) {
+        Level L;
+        L.n = cur;
+        L.m = kInternalM;
+        L.K = plan_blocks(cur, L.m);
+        const int64_t last_len = cur - (L.K - 1) * L.m;
+        L.kfull = (last_len == L.m) ? L.K : L.K - 1;
+        L.tail = (last_len == L.m) ? 0 : last_len;
+        L.internal = true;
+        ws += 5 * pad32((size_t)(2 * L.K));
+        p.levels.push_back(L);
+        cur = 2 * L.K;
+    }
+    p.n_final = cur;
+    p.ws_doubles = ws;
+    return true;
+}
+
+void bind_plan(Plan& p, const SysPtrs& sys, double* x, double* ws) {
+    SysPtrs in = sys;
+    double* xo = x;
+    double* w = ws;
+    for (auto& L : p.levels) {
+        L.in = in;
+        L.x_out = xo;
+        const size_t k2 = pad32((size_t)(2 * L.K));
+        L.iface.sub = w;
+        L.iface.diag = w + k2;
+        L.iface.sup = w + 2 * k2;
+        L.iface.rhs = w + 3 * k2;
+        L.x_iface = w + 4 * k2;
+        w += 5 * k2;
+        in = SysPtrs{L.iface.sub, L.iface.diag, L.iface.sup, L.iface.rhs};
+        xo = L.x_iface;
+    }
+    p.final_in = in;
+    p.final_x = xo;
+}
+
+int generic_G(int64_t blen, int tmax) {
+    int G = 1;
+    while (G * 2 <= tmax && blen / (G * 2) >= 4) G *= 2;
+    return G;
+}
+
+bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
+
+}  // namespace
+
+struct tp_obs_set;
+
+struct tp_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    bool graphs = true;
+    double* ws = nullptr;
+    size_t ws_cap = 0;  // doubles
+    unsigned long long* d_err = nullptr;
+    unsigned long long* h_err = nullptr;
+    unsigned long long* d_red = nullptr;  // residual / scratch words
+    double* d_small = nullptr;            // shard scratch (x2 + gather scratch)
+    double* dsys = nullptr;               // host-path staging (5 arrays)
+    size_t dsys_cap = 0;                  // rows
+    int64_t last_launches = 0;
+    std::vector<std::pair<int64_t, int>> occ;  // (key, grid cap)
+    struct GraphEntry {
+        std::vector<int64_t> key;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        uint64_t stamp = 0;
+    };
+    std::vector<GraphEntry> gcache;
+    uint64_t clock = 0;
+};
+
+namespace {
+
+int fast_grid_cap(tp_ctx* ctx, int64_t m, bool vec, int mode) {
+    const int64_t key = (m << 2) | (vec ? 2 : 0) | mode;
+    for (auto& kv : ctx->occ)
+        if (kv.first == key) return kv.second;
+    int nb = tpb::fast_max_active_blocks(m, vec, mode);
+    if (nb < 1) nb = 1;
+    const int cap = nb * ctx->sms;
+    ctx->occ.push_back({key, cap});
+    return cap;
+}
+
+using KernelHook = void (*)(void* user, const char* name);
+
+struct Runner {
+    tp_ctx* ctx;
+    cudaStream_t st;
+    KernelHook hook = nullptr;
+    void* hook_user = nullptr;
+    int64_t launches = 0;
+    cudaError_t status = cudaSuccess;
+
+    void after(const char* what, int level) {
+        ++launches;
+        if (hook) {
+            char name[32];
+            std::snprintf(name, sizeof(name), "%s:L%d", what, level);
+            hook(hook_user, name);
+        }
+    }
+    void check(cudaError_t e) {
+        if (e != cudaSuccess && status == cudaSuccess) status = e;
+    }
+
+    void stage(const Level& L, int level, int mode) {
+        const bool s1 = (mode == tpb::kStage1);
+        if (L.kfull > 0) {
+            int fl, fg;
+            if (tpb::fast_shape(L.m, &fl, &fg)) {
+                const bool vec = aligned32(L.in.sub) && aligned32(L.in.diag) && aligned32(L.in.sup) &&
+                                 aligned32(L.in.rhs) && (s1 || aligned32(L.x_out));
+                check(tpb::launch_fast(L.m, vec, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
+                                       ctx->d_err, level, fast_grid_cap(ctx, L.m, vec, mode), st));
+                after(s1 ? "stage1" : "stage3", level);
+            } else {
+                const int T = tpb::kGenericThreads;
+                const int G = generic_G(L.m, T);
+                const int64_t bpc = T / G;
+                int64_t grid = (L.kfull + bpc - 1) / bpc;
+                grid = std::min<int64_t>(grid, (int64_t)ctx->sms * 8);
+                check(tpb::launch_generic(mode, T, G, (int)grid, L.in, 0, 0, L.kfull, L.m, L.iface,
+                                          L.x_iface, L.x_out, ctx->d_err, level, st));
+                after(s1 ? "stage1g" : "stage3g", level);
+            }
+        }
+        if (L.tail > 0) {
+            const int G = generic_G(L.tail, tpb::kGenericThreads);
+            const int T = std::max(32, G);
+            check(tpb::launch_generic(mode, T, G, 1, L.in, L.kfull * L.m, L.kfull, 1, L.tail, L.iface,
+                                      L.x_iface, L.x_out, ctx->d_err, level, st));
+            after(s1 ? "stage1t" : "stage3t", level);
+        }
+    }
+
+    void final_solve(const Plan& p) {
+        const int G = generic_G(p.n_final, tpb::kFinalThreads);
+        const int T = std::max(32, G);
+        check(tpb::launch_generic(tpb::kSolve, T, G, 1, p.final_in, 0, 0, 1, p.n_final, IfacePtrs{},
+                                  nullptr, p.final_x, ctx->d_err, (int)p.levels.size(), st));
+        after("final", (int)p.levels.size());
+    }
+
+    // Whole solve (reset error word, Stage 1 down, finish, Stage 3 up).
+    void solve(const Plan& p) {
+        check(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
+        for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
+        final_solve(p);
+        for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
+    }
+
+    // Sharded halves.
+    void shard_reduce(const Plan& p, double* eq8) {
+        check(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
+        for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
+        const int G = generic_G(p.n_final, tpb::kFinalThreads);
+        const int T = std::max(32, G);
+        IfacePtrs o{eq8, eq8 + 2, eq8 + 4, eq8 + 6};
+        check(tpb::launch_generic(tpb::kStage1, T, G, 1, p.final_in, 0, 0, 1, p.n_final, o, nullptr,
+                                  nullptr, ctx->d_err, (int)p.levels.size(), st));
+        after("shard_reduce", (int)p.levels.size());
+    }
+    void shard_finish(const Plan& p, const double* eq_all, int nranks, int rank) {
+        double* x2 = ctx->d_small;
+        double* scratch = ctx->d_small + 32;
+        check(tpb::launch_gather_solve(eq_all, nranks, rank, x2, scratch, ctx->d_err,
+                                       (int)p.levels.size() + 1, st));
+        after("gather_solve", (int)p.levels.size() + 1);
+        const int G = generic_G(p.n_final, tpb::kFinalThreads);
+        const int T = std::max(32, G);
+        check(tpb::launch_generic(tpb::kStage3, T, G, 1, p.final_in, 0, 0, 1, p.n_final, IfacePtrs{},
+                                  x2, p.final_x, ctx->d_err, (int)p.levels.size(), st));
+        after("shard_expand", (int)p.levels.size());
+        for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
+    }
+};
+
+tp_status validate_policy(int64_t n, const int64_t* sizes, int32_t nsizes, tp_error* err) {
+    // RecursionPolicy::valid — partition.hpp:181-186, checked first (:239)
+    if (nsizes < 1 || sizes == nullptr) {
+        set_err(err, TP_ERR_INVALID_SIZE, "invalid recursion policy");
+        return TP_ERR_INVALID_SIZE;
+    }
+    for (int i = 0; i < nsizes; ++i)
+        if (sizes[i] < 2) {
+            set_err(err, TP_ERR_INVALID_SIZE, "invalid recursion policy");
+            return TP_ERR_INVALID_SIZE;
+        }
+    if (n <= 0) {  // :240
+        set_err(err, TP_ERR_INVALID_SIZE, "empty system");
+        return TP_ERR_INVALID_SIZE;
+    }
+    return TP_OK;
+}
+
+tp_status validate(const double* a, const double* b, const double* c, const double* d, int64_t n,
+                   const int64_t* sizes, int32_t nsizes, const double* x, tp_error* err) {
+    tp_status s = validate_policy(n, sizes, nsizes, err);
+    if (s != TP_OK) return s;
+    if (!a || !b || !c || !d || !x) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null array pointer");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    return TP_OK;
+}
+
+tp_status ensure_ws(tp_ctx* ctx, size_t doubles, tp_error* err) {
+    if (doubles <= ctx->ws_cap) return TP_OK;
+    // growing the workspace invalidates every captured graph
+    for (auto& g : ctx->gcache) cudaGraphExecDestroy(g.exec);
+    ctx->gcache.clear();
+    if (ctx->ws) cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_cap = 0;
+    const size_t want = doubles + doubles / 8 + 1024;
+    TP_CUDA(cudaMalloc(&ctx->ws, want * sizeof(double)));
+    ctx->ws_cap = want;
+    return TP_OK;
+}
+
+tp_status decode_device_error(tp_ctx* ctx, tp_error* err) {
+    const unsigned long long code = *ctx->h_err;
+    if (code == tpb::kNoError) return TP_OK;
+    const int32_t level = (int32_t)(code >> 48);
+    const int64_t row = (int64_t)(code & 0xFFFFFFFFFFFFULL);
+    set_err(err, TP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(row), row, level);
+    return TP_ERR_ZERO_PIVOT;
+}
+
+// Runs `fn(runner)` directly or through a cached CUDA graph keyed by `key`.
+template <class Fn>
+tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_t>& key, Fn&& fn,
+                          tp_error* err) {
+    if (!ctx->graphs) {
+        Runner r{ctx, st};
+        fn(r);
+        ctx->last_launches = r.launches;
+        if (r.status != cudaSuccess) {
+            set_err(err, TP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(r.status));
+            return TP_ERR_CUDA;
+        }
+        return TP_OK;
+    }
+    for (auto& g : ctx->gcache) {
+        if (g.key == key) {
+            g.stamp = ++ctx->clock;
+            TP_CUDA(cudaGraphLaunch(g.exec, st));
+            ctx->last_launches = g.launches;
+            return TP_OK;
+        }
+    }
+    cudaStream_t cap = st;
+    bool own_cap = false;
+    if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) {
+        // the legacy stream cannot be captured: capture on a private stream
+        TP_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        own_cap = true;
+    }
+    TP_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    Runner r{ctx, cap};
+    fn(r);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+    if (r.status != cudaSuccess || ce != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        if (own_cap) cudaStreamDestroy(cap);
+        set_err(err, TP_ERR_CUDA,
+                std::string("graph capture: ") +
+                    cudaGetErrorString(r.status != cudaSuccess ? r.status : ce));
+        return TP_ERR_CUDA;
+    }
+    if (own_cap) cudaStreamDestroy(cap);
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+        set_err(err, TP_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+        return TP_ERR_CUDA;
+    }
+    if (ctx->gcache.size() >= 16) {
+        auto it = std::min_element(ctx->gcache.begin(), ctx->gcache.end(),
+                                   [](const auto& x, const auto& y) { return x.stamp < y.stamp; });
+        cudaGraphExecDestroy(it->exec);
+        ctx->gcache.erase(it);
+    }
+    tp_ctx::GraphEntry ge;
+    ge.key = key;
+    ge.exec = exec;
+    ge.launches = r.launches;
+    ge.stamp = ++ctx->clock;
+    ctx->gcache.push_back(ge);
+    ctx->last_launches = r.launches;
+    TP_CUDA(cudaGraphLaunch(exec, st));
+    return TP_OK;
+}
+
+std::vector<int64_t> make_key(int64_t tag, int64_t n, const int64_t* sizes, int32_t nsizes,
+                              std::initializer_list<const void*> ptrs, int64_t extra = 0) {
+    std::vector<int64_t> k;
+    k.push_back(tag);
+    k.push_back(n);
+    k.push_back(extra);
+    for (int i = 0; i < nsizes; ++i) k.push_back(sizes[i]);
+    k.push_back(-1);
+    for (const void* p : ptrs) k.push_back((int64_t) reinterpret_cast<uintptr_t>(p));
+    return k;
+}
+
+cudaStream_t pick_stream(tp_ctx* ctx, void* s) {
+    return s ? static_cast<cudaStream_t>(s) : ctx->stream;
+}
+
+tp_status ensure_dsys(tp_ctx* ctx, int64_t n, tp_error* err) {
+    if ((size_t)n <= ctx->dsys_cap) return TP_OK;
+    for (auto& g : ctx->gcache) cudaGraphExecDestroy(g.exec);
+    ctx->gcache.clear();
+    if (ctx->dsys) cudaFree(ctx->dsys);
+    ctx->dsys = nullptr;
+    ctx->dsys_cap = 0;
+    const size_t rows = pad32((size_t)n);
+    TP_CUDA(cudaMalloc(&ctx->dsys, 5 * rows * sizeof(double)));
+    ctx->dsys_cap = rows;
+    return TP_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+extern "C" {
+
+int32_t tp_abi_version(void) { return TP_ABI_VERSION; }
+
+tp_status tp_ctx_create(int32_t device, tp_ctx** out, tp_error* err) {
+    clear_err(err);
+    if (!out) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "out is NULL");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    int ndev = 0;
+    TP_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "device index out of range");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    TP_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0) {
+        set_err(err, TP_ERR_CUDA,
+                "tridpart_b200 is built for sm_100a (B200); found sm_" + std::to_string(prop.major) +
+                    std::to_string(prop.minor));
+        return TP_ERR_CUDA;
+    }
+    TP_CUDA(tpb::init_kernel_attributes());
+    tp_ctx* c = new tp_ctx();
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 64);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_red, 64);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_small, 4096);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_err, 64);
+    if (e != cudaSuccess) {
+        set_err(err, TP_ERR_CUDA, std::string("context allocation: ") + cudaGetErrorString(e));
+        tp_ctx_destroy(c);
+        return TP_ERR_CUDA;
+    }
+    c->stream = c->own;
+    *out = c;
+    return TP_OK;
+}
+
+void tp_ctx_destroy(tp_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (auto& g : ctx->gcache) cudaGraphExecDestroy(g.exec);
+    if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->dsys) cudaFree(ctx->dsys);
+    if (ctx->d_err) cudaFree(ctx->d_err);
+    if (ctx->d_red) cudaFree(ctx->d_red);
+    if (ctx->d_small) cudaFree(ctx->d_small);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+tp_status tp_ctx_set_stream(tp_ctx* ctx, void* stream, tp_error* err) {
+    clear_err(err);
+    if (!ctx) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    return TP_OK;
+}
+
+tp_status tp_ctx_set_graphs(tp_ctx* ctx, int32_t enabled, tp_error* err) {
+    clear_err(err);
+    if (!ctx) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    ctx->graphs = enabled != 0;
+    return TP_OK;
+}
+
+int64_t tp_ctx_last_launch_count(const tp_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+tp_status tp_solve_partition_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                     const double* super, const double* rhs, int64_t n,
+                                     const int64_t* sizes, int32_t nsizes, double* x, void* stream,
+                                     tp_error* err) {
+    clear_err(err);
+    if (!ctx) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaSetDevice(ctx->device));
+    Plan p;
+    build_plan(n, sizes, nsizes, p);
+    s = ensure_ws(ctx, p.ws_doubles, err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs{sub, diag, super, rhs}, x, ctx->ws);
+    const cudaStream_t st = pick_stream(ctx, stream);
+    auto key = make_key(1, n, sizes, nsizes, {sub, diag, super, rhs, x, ctx->ws});
+    return run_maybe_graph(ctx, st, key, [&](Runner& r) { r.solve(p); }, err);
+}
+
+tp_status tp_check_device_error(tp_ctx* ctx, tp_error* err) {
+    clear_err(err);
+    if (!ctx) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaMemcpy(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return decode_device_error(ctx, err);
+}
+
+tp_status tp_solve_partition_f64(tp_ctx* ctx, const double* sub, const double* diag,
+                                 const double* super, const double* rhs, int64_t n,
+                                 const int64_t* sizes, int32_t nsizes, double* x, tp_error* err) {
+    clear_err(err);
+    if (!ctx) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaSetDevice(ctx->device));
+    s = ensure_dsys(ctx, n, err);
+    if (s != TP_OK) return s;
+    const size_t rows = ctx->dsys_cap;
+    double* da = ctx->dsys;
+    double* db = da + rows;
+    double* dc = db + rows;
+    double* dd = dc + rows;
+    double* dx = dd + rows;
+    const cudaStream_t st = ctx->stream;
+    const size_t bytes = (size_t)n * sizeof(double);
+    TP_CUDA(cudaMemcpyAsync(da, sub, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(db, diag, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(dc, super, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(dd, rhs, bytes, cudaMemcpyHostToDevice, st));
+    s = tp_solve_partition_f64_dev(ctx, da, db, dc, dd, n, sizes, nsizes, dx, st, err);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaStreamSynchronize(st));
+    return decode_device_error(ctx, err);
+}
+
+tp_status tp_solve_partition_observe_f64(tp_ctx* ctx, const double* sub, const double* diag,
+                                         const double* super, const double* rhs, int64_t n,
+                                         const int64_t* sizes, int32_t nsizes, double* x,
+                                         tp_interface_cb cb, void* user, tp_error* err) {
+    tp_status s = tp_solve_partition_f64(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    if (s != TP_OK || cb == nullptr) return s;
+    Plan p;
+    build_plan(n, sizes, nsizes, p);
+    bind_plan(p, SysPtrs{ctx->dsys, ctx->dsys + ctx->dsys_cap, ctx->dsys + 2 * ctx->dsys_cap,
+                         ctx->dsys + 3 * ctx->dsys_cap},
+              ctx->dsys + 4 * ctx->dsys_cap, ctx->ws);
+    std::vector<double> h;
+    for (size_t l = 0; l < p.levels.size(); ++l) {
+        const Level& L = p.levels[l];
+        if (L.internal) break;  // device-internal levels are not part of the policy
+        const int64_t n2 = 2 * L.K;
+        h.resize((size_t)(4 * n2));
+        TP_CUDA(cudaMemcpy(h.data(), L.iface.sub, n2 * sizeof(double), cudaMemcpyDeviceToHost));
+        TP_CUDA(cudaMemcpy(h.data() + n2, L.iface.diag, n2 * sizeof(double), cudaMemcpyDeviceToHost));
+        TP_CUDA(cudaMemcpy(h.data() + 2 * n2, L.iface.sup, n2 * sizeof(double), cudaMemcpyDeviceToHost));
+        TP_CUDA(cudaMemcpy(h.data() + 3 * n2, L.iface.rhs, n2 * sizeof(double), cudaMemcpyDeviceToHost));
+        cb((int64_t)l, n2, h.data(), h.data() + n2, h.data() + 2 * n2, h.data() + 3 * n2, user);
+    }
+    return TP_OK;
+}
+
+tp_status tp_thomas_solve_f64(tp_ctx* ctx, const double* sub, const double* diag,
+                              const double* super, const double* rhs, int64_t n, double* x,
+                              tp_error* err) {
+    // A policy with no partition levels: n >= 4 still needs one level of m >= n
+    // for the reference planner, so drive the finishing solver directly.
+    clear_err(err);
+    if (!ctx) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    if (n <= 0) {
+        set_err(err, TP_ERR_INVALID_SIZE, "empty system");
+        return TP_ERR_INVALID_SIZE;
+    }
+    if (!sub || !diag || !super || !rhs || !x) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null array pointer");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    tp_status s = ensure_dsys(ctx, n, err);
+    if (s != TP_OK) return s;
+    const size_t rows = ctx->dsys_cap;
+    double* da = ctx->dsys;
+    double* db = da + rows;
+    double* dc = db + rows;
+    double* dd = dc + rows;
+    double* dx = dd + rows;
+    const cudaStream_t st = ctx->stream;
+    const size_t bytes = (size_t)n * sizeof(double);
+    TP_CUDA(cudaMemcpyAsync(da, sub, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(db, diag, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(dc, super, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(dd, rhs, bytes, cudaMemcpyHostToDevice, st));
+    // no policy levels: only device-internal levels (if n is large) + finish
+    Plan p;
+    build_plan(n, nullptr, 0, p);
+    s = ensure_ws(ctx, p.ws_doubles, err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs{da, db, dc, dd}, dx, ctx->ws);
+    auto key = make_key(2, n, nullptr, 0, {da, db, dc, dd, dx, ctx->ws});
+    s = run_maybe_graph(ctx, st, key, [&](Runner& r) { r.solve(p); }, err);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaStreamSynchronize(st));
+    return decode_device_error(ctx, err);
+}
+
+tp_status tp_residual_inf_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                  const double* super, const double* rhs, int64_t n,
+                                  const double* x, double* out, tp_error* err) {
+    clear_err(err);
+    if (!ctx || !out || !sub || !diag || !super || !rhs || !x) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    const cudaStream_t st = ctx->stream;
+    TP_CUDA(cudaMemsetAsync(ctx->d_red, 0, 2 * sizeof(unsigned long long), st));
+    TP_CUDA(tpb::launch_residual(SysPtrs{sub, diag, super, rhs}, n, x, ctx->d_red, ctx->sms, st));
+    unsigned long long h[2];
+    TP_CUDA(cudaMemcpyAsync(h, ctx->d_red, sizeof(h), cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaStreamSynchronize(st));
+    double num, den;
+    std::memcpy(&num, &h[0], sizeof(double));
+    std::memcpy(&den, &h[1], sizeof(double));
+    if (den < 1.0) den = 1.0;
+    *out = num / den;
+    return TP_OK;
+}
+
+tp_status tp_shard_reduce_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                  const double* super, const double* rhs, int64_t n_local,
+                                  const int64_t* sizes, int32_t nsizes, double* eq8_dev,
+                                  void* stream, tp_error* err) {
+    clear_err(err);
+    if (!ctx || !eq8_dev) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    tp_status s = validate(sub, diag, super, rhs, n_local, sizes, nsizes, eq8_dev, err);
+    if (s != TP_OK) return s;
+    if (n_local < 2) {
+        set_err(err, TP_ERR_INVALID_SIZE, "a shard needs at least 2 rows");
+        return TP_ERR_INVALID_SIZE;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    Plan p;
+    build_plan(n_local, sizes, nsizes, p);
+    s = ensure_ws(ctx, p.ws_doubles, err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs{sub, diag, super, rhs}, nullptr, ctx->ws);
+    const cudaStream_t st = pick_stream(ctx, stream);
+    auto key = make_key(3, n_local, sizes, nsizes, {sub, diag, super, rhs, eq8_dev, ctx->ws});
+    return run_maybe_graph(ctx, st, key, [&](Runner& r) { r.shard_reduce(p, eq8_dev); }, err);
+}
+
+tp_status tp_shard_finish_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                  const double* super, const double* rhs, int64_t n_local,
+                                  const int64_t* sizes, int32_t nsizes, const double* eq_all_dev,
+                                  int32_t nranks, int32_t rank, double* x_dev, void* stream,
+                                  tp_error* err) {
+    clear_err(err);
+    if (!ctx || !eq_all_dev) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    if (nranks < 1 || nranks > 1024 || rank < 0 || rank >= nranks) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "bad rank / nranks");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    tp_status s = validate(sub, diag, super, rhs, n_local, sizes, nsizes, x_dev, err);
+    if (s != TP_OK) return s;
+    if (n_local < 2) {
+        set_err(err, TP_ERR_INVALID_SIZE, "a shard needs at least 2 rows");
+        return TP_ERR_INVALID_SIZE;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    if (4 * nranks + 64 > 512) {
+        // d_small holds 32 + 4*nranks doubles of scratch
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "too many ranks for the scratch buffer");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    Plan p;
+    build_plan(n_local, sizes, nsizes, p);
+    s = ensure_ws(ctx, p.ws_doubles, err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs{sub, diag, super, rhs}, x_dev, ctx->ws);
+    const cudaStream_t st = pick_stream(ctx, stream);
+    auto key = make_key(4, n_local, sizes, nsizes, {sub, diag, super, rhs, eq_all_dev, x_dev, ctx->ws},
+                        ((int64_t)nranks << 32) | rank);
+    return run_maybe_graph(ctx, st, key,
+                           [&](Runner& r) { r.shard_finish(p, eq_all_dev, nranks, rank); }, err);
+}
+
+tp_status tp_generate_system_f64_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global,
+                                     uint64_t seed, double delta, double* sub, double* diag,
+                                     double* super, double* rhs, void* stream, tp_error* err) {
+    clear_err(err);
+    if (!ctx || !sub || !diag || !super || !rhs) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    if (n_global < 2 || n < 0 || row0 < 0 || row0 + n > n_global) {  // bench.hpp:69
+        set_err(err, TP_ERR_INVALID_SIZE, "system size must be >= 2");
+        return TP_ERR_INVALID_SIZE;
+    }
+    if (!(delta > 1.0)) {  // bench.hpp:70
+        set_err(err, TP_ERR_INVALID_SIZE, "dominance factor must be > 1");
+        return TP_ERR_INVALID_SIZE;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    TP_CUDA(tpb::launch_generate(n, row0, n_global, seed, delta, sub, diag, super, rhs, ctx->sms,
+                                 pick_stream(ctx, stream)));
+    return TP_OK;
+}
+
+tp_status tp_make_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* nblocks, tp_error* err) {
+    clear_err(err);
+    if (n < 2) {
+        set_err(err, TP_ERR_INVALID_SIZE, "system size must be >= 2");
+        return TP_ERR_INVALID_SIZE;
+    }
+    if (m < 2) {
+        set_err(err, TP_ERR_INVALID_SIZE, "sub-system size must be >= 2");
+        return TP_ERR_INVALID_SIZE;
+    }
+    const int64_t K = plan_blocks(n, m);
+    if (nblocks) *nblocks = K;
+    if (bounds) {
+        for (int64_t j = 0; j < K; ++j) bounds[j] = j * m;
+        bounds[K] = n;
+    }
+    return TP_OK;
+}
+
+tp_status tp_plan_levels(int64_t n, const int64_t* sizes, int32_t nsizes, int64_t* level_n,
+                         int64_t* level_m, int32_t* nlevels, int32_t max_levels, int64_t* n_final,
+                         tp_error* err) {
+    clear_err(err);
+    tp_status s = validate_policy(n, sizes, nsizes, err);
+    if (s != TP_OK) return s;
+    Plan p;
+    build_plan(n, sizes, nsizes, p);
+    if ((int32_t)p.levels.size() > max_levels) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "max_levels too small");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    for (size_t l = 0; l < p.levels.size(); ++l) {
+        if (level_n) level_n[l] = p.levels[l].n;
+        if (level_m) level_m[l] = p.levels[l].internal ? -p.levels[l].m : p.levels[l].m;
+    }
+    if (nlevels) *nlevels = (int32_t)p.levels.size();
+    if (n_final) *n_final = p.n_final;
+    return TP_OK;
+}
+
+struct ProfileState {
+    cudaStream_t st;
+    std::vector<cudaEvent_t> evs;
+    std::vector<std::string> names;
+};
+
+static void profile_hook(void* user, const char* name) {
+    auto* ps = static_cast<ProfileState*>(user);
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, ps->st);
+    ps->evs.push_back(e);
+    ps->names.push_back(name);
+}
+
+tp_status tp_solve_profile_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                   const double* super, const double* rhs, int64_t n,
+                                   const int64_t* sizes, int32_t nsizes, double* x, float* kernel_ms,
+                                   char* names, int32_t max_kernels, int32_t* nkernels,
+                                   tp_error* err) {
+    clear_err(err);
+    if (!ctx) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaSetDevice(ctx->device));
+    Plan p;
+    build_plan(n, sizes, nsizes, p);
+    s = ensure_ws(ctx, p.ws_doubles, err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs{sub, diag, super, rhs}, x, ctx->ws);
+    const cudaStream_t st = ctx->stream;
+    ProfileState ps{st, {}, {}};
+    cudaEvent_t e0;
+    TP_CUDA(cudaEventCreate(&e0));
+    TP_CUDA(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
+    TP_CUDA(cudaEventRecord(e0, st));
+    Runner r{ctx, st};
+    r.hook = profile_hook;
+    r.hook_user = &ps;
+    for (size_t l = 0; l < p.levels.size(); ++l) r.stage(p.levels[l], (int)l, tpb::kStage1);
+    r.final_solve(p);
+    for (size_t l = p.levels.size(); l-- > 0;) r.stage(p.levels[l], (int)l, tpb::kStage3);
+    ctx->last_launches = r.launches;
+    TP_CUDA(cudaStreamSynchronize(st));
+    const int32_t cnt = (int32_t)std::min<size_t>(ps.evs.size(), (size_t)max_kernels);
+    cudaEvent_t prev = e0;
+    for (int32_t i = 0; i < cnt; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, prev, ps.evs[i]);
+        if (kernel_ms) kernel_ms[i] = ms;
+        if (names) std::snprintf(names + 32 * i, 32, "%s", ps.names[i].c_str());
+        prev = ps.evs[i];
+    }
+    if (nkernels) *nkernels = cnt;
+    for (auto e : ps.evs) cudaEventDestroy(e);
+    cudaEventDestroy(e0);
+    if (r.status != cudaSuccess) {
+        set_err(err, TP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(r.status));
+        return TP_ERR_CUDA;
+    }
+    return TP_OK;
+}
+
+}  // extern "C"

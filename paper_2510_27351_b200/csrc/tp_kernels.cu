@@ -1,0 +1,572 @@
+// sm_100a kernels of the B200 partition solver (FP64, HBM-bound).
+//
+// Kernel map (reference call stack partition.hpp:191-224):
+//   k_fast<L,G,STAGE1>   parallel_for(reduce_block) + assemble_interface   :203-205
+//   k_fast<L,G,STAGE3>   parallel_for(back_substitute + scatter)            :214-222
+//   k_generic<MODE>      the same for any block length (tail blocks, odd m),
+//                        and the single-CTA finishing solve that replaces
+//                        thomas_solve(iface) at the deepest level          :208-211
+//   k_gather_solve       sharded top level: Thomas on the all-gathered 2P rows
+//   k_generate           device-side counter-based generate_system analogue
+//   k_residual           residual_inf (tridiagonal.hpp:74-87)
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tp_device.cuh"
+#include "tp_kernels.h"
+
+namespace tpb {
+
+// ===========================================================================
+// Fast path: full blocks of m = L*G rows, one chunk of L rows per thread held
+// in registers, G lanes per block (G | 32), lane-tree merges via shuffles.
+// ===========================================================================
+template <int L, int G, int MODE, bool VEC>
+__global__ void __launch_bounds__(kFastThreads) k_fast(SysPtrs sys, int64_t nblocks, IfacePtrs out,
+                                                       const double* __restrict__ xi,
+                                                       double* __restrict__ x,
+                                                       unsigned long long* err, int level) {
+    static_assert(32 % G == 0, "G must divide the warp");
+    constexpr int LOGG = (G >= 32) ? 5 : (G >= 16) ? 4 : (G >= 8) ? 3 : (G >= 4) ? 2 : (G >= 2) ? 1 : 0;
+    const int64_t nchunks = nblocks * G;
+    const int lane = threadIdx.x & 31;
+    const int c = lane % G;  // chunk index inside the block
+    int64_t bad = INT64_MAX;
+
+    for (int64_t base = (int64_t)blockIdx.x * kFastThreads; base < nchunks;
+         base += (int64_t)gridDim.x * kFastThreads) {
+        const int64_t t = base + threadIdx.x;
+        // warp-uniform liveness: groups never straddle the nchunks boundary
+        const bool active = t < nchunks;
+        const int64_t row0 = t * L;
+        Chunk<L> r;
+        if (active) {
+            load_rows<L, VEC>(sys.sub, row0, r.a);
+            load_rows<L, VEC>(sys.diag, row0, r.b);
+            load_rows<L, VEC>(sys.sup, row0, r.c);
+            load_rows<L, VEC>(sys.rhs, row0, r.d);
+        } else {
+#pragma unroll
+            for (int i = 0; i < L; ++i) { r.a[i] = 0; r.b[i] = 1; r.c[i] = 0; r.d[i] = 0; }
+        }
+        const int64_t blk = t / G;
+
+        if constexpr (MODE == kStage1) {
+            int64_t lbad = INT64_MAX;
+            Eq2 cur = leaf_reduce<L>(r, L, row0, lbad);
+#pragma unroll
+            for (int lv = 0; lv < LOGG; ++lv) {
+                const int h = 1 << lv;
+                const Eq2 oth = shfl_down_eq(cur, h);
+                if ((c & (2 * h - 1)) == 0) {
+                    MergeSave sv;
+                    cur = merge(cur, oth, row0 + (int64_t)h * L - 1, lbad, sv);
+                }
+            }
+            if (active) {
+                bad = lbad < bad ? lbad : bad;
+                if (c == 0) {
+                    const int64_t o = 2 * blk;
+                    *reinterpret_cast<double2*>(out.sub + o) = make_double2(cur.a1, cur.a2);
+                    *reinterpret_cast<double2*>(out.diag + o) = make_double2(cur.b1, cur.b2);
+                    *reinterpret_cast<double2*>(out.sup + o) = make_double2(cur.g1, cur.g2);
+                    *reinterpret_cast<double2*>(out.rhs + o) = make_double2(cur.d1, cur.d2);
+                }
+            }
+        } else {
+            int64_t lbad = INT64_MAX;
+            double rbeta[L], gam[L], del[L];
+            Eq2 cur = leaf_reduce_keep<L>(r, L, row0, lbad, rbeta, gam, del);
+            MergeSave sv[LOGG > 0 ? LOGG : 1];
+#pragma unroll
+            for (int lv = 0; lv < LOGG; ++lv) {
+                const int h = 1 << lv;
+                const Eq2 oth = shfl_down_eq(cur, h);
+                if ((c & (2 * h - 1)) == 0) cur = merge(cur, oth, row0 + (int64_t)h * L - 1, lbad, sv[lv]);
+            }
+            // block ends from the next level's solution
+            double xs = 0, xe = 0;
+            if (c == 0 && active) {
+                const double2 v = *reinterpret_cast<const double2*>(xi + 2 * blk);
+                xs = v.x;
+                xe = v.y;
+            }
+#pragma unroll
+            for (int lv = LOGG - 1; lv >= 0; --lv) {
+                const int h = 1 << lv;
+                double xt = 0;
+                if ((c & (2 * h - 1)) == 0) xt = merge_xt(sv[lv], xs, xe);
+                const double rxt = __shfl_up_sync(0xffffffffu, xt, h);
+                const double rxe = __shfl_up_sync(0xffffffffu, xe, h);
+                if ((c & (2 * h - 1)) == h) {
+                    xs = first_from_e1(cur, rxt, rxe);
+                    xe = rxe;
+                } else if ((c & (2 * h - 1)) == 0) {
+                    xe = xt;
+                }
+            }
+            double xv[L];
+            leaf_expand<L>(r, L, rbeta, gam, del, xs, xe, xv);
+            if (active) {
+                bad = lbad < bad ? lbad : bad;
+                store_rows<L, VEC>(x, row0, xv);
+            }
+        }
+    }
+    report_pivot(err, level, bad);
+}
+
+// ===========================================================================
+// Generic path: any block length, rows staged through shared memory.
+// CTA of T threads; G lanes per block (G power of two, G <= T); each lane owns
+// a chunk of floor/ceil(blen/G) >= 2 rows. Lane-tree via shuffles below the
+// warp, via shared memory above it.
+// ===========================================================================
+struct GenShared {
+    double* a;
+    double* b;
+    double* c;
+    double* d;
+    Eq2* xeq;       // one slot per warp (cross-warp merges)
+    double* xpass;  // 2 per warp (cross-warp top-down)
+};
+
+// Leaf on a shared-memory chunk [p, p+len). When KEEP, overwrites b <- rcp(beta),
+// c <- gamma, d <- delta for the interior rows (consumed by leaf expansion).
+template <bool KEEP>
+__device__ Eq2 leaf_smem(double* a, double* b, double* c, double* d, int len, int64_t grow0,
+                         int64_t& bad) {
+    Eq2 q;
+    if (len == 1) {  // only in the n == 1 solve
+        q.a1 = a[0]; q.b1 = b[0]; q.g1 = c[0]; q.d1 = d[0];
+        q.a2 = a[0]; q.b2 = b[0]; q.g2 = c[0]; q.d2 = d[0];
+        return q;
+    }
+    // down-sweep first (reads originals): partition.hpp:110-124
+    double phi = a[1], bp = b[1], dp = d[1];
+    for (int i = 2; i < len; ++i) {
+        check_pivot(bp, grow0 + i - 1, bad);
+        const double w = a[i] * rcp(bp);
+        phi = -w * phi;
+        bp = b[i] - w * c[i - 1];
+        dp = d[i] - w * dp;
+    }
+    q.a2 = phi;
+    q.b2 = bp;
+    q.g2 = c[len - 1];
+    q.d2 = dp;
+    // up-sweep: partition.hpp:90-108
+    double beta = b[len - 2], gamma = c[len - 2], delta = d[len - 2];
+    if (KEEP) { c[len - 2] = gamma; d[len - 2] = delta; }
+    for (int i = len - 3; i >= 0; --i) {
+        check_pivot(beta, grow0 + i + 1, bad);
+        const double rb = rcp(beta);
+        const double w = c[i] * rb;
+        const double nb = b[i] - w * a[i + 1];
+        const double ng = -w * gamma;
+        const double nd = d[i] - w * delta;
+        if (KEEP) { b[i + 1] = rb; c[i] = ng; d[i] = nd; }
+        beta = nb; gamma = ng; delta = nd;
+    }
+    q.a1 = a[0];
+    q.b1 = beta;
+    q.g1 = gamma;
+    q.d1 = delta;
+    return q;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t row_base, int64_t blk_base, int64_t nblocks,
+                          int64_t blen, int G, IfacePtrs out, const double* __restrict__ xi,
+                          double* __restrict__ x, unsigned long long* err, int level) {
+    extern __shared__ __align__(16) double gsm[];
+    const int T = blockDim.x;
+    const int bpc = T / G;
+    const int64_t tile_rows_max = (int64_t)bpc * blen;
+    GenShared s;
+    s.a = gsm;
+    s.b = s.a + tile_rows_max;
+    s.c = s.b + tile_rows_max;
+    s.d = s.c + tile_rows_max;
+    s.xeq = reinterpret_cast<Eq2*>(s.d + tile_rows_max);
+    s.xpass = reinterpret_cast<double*>(s.xeq + (T + 31) / 32);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int c = tid % G;
+    const int lb = tid / G;
+    const int64_t Llo = blen / G;
+    const int64_t ext = blen % G;
+    const int len = (int)(Llo + (c < ext ? 1 : 0));
+    const int64_t off = c * Llo + (c < ext ? c : ext);
+    int logg = 0;
+    while ((1 << logg) < G) ++logg;
+    int64_t bad = INT64_MAX;
+    constexpr bool KEEP = (MODE != kStage1);
+
+    const int64_t ntiles = (nblocks + bpc - 1) / bpc;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t b0 = tile * bpc;
+        const int64_t nbt = (nblocks - b0) < bpc ? (nblocks - b0) : bpc;
+        const int64_t trow0 = row_base + b0 * blen;
+        const int64_t trows = nbt * blen;
+        for (int64_t i = tid; i < trows; i += T) {
+            s.a[i] = sys.sub[trow0 + i];
+            s.b[i] = sys.diag[trow0 + i];
+            s.c[i] = sys.sup[trow0 + i];
+            s.d[i] = sys.rhs[trow0 + i];
+        }
+        __syncthreads();
+        const bool active = lb < nbt;
+        const int64_t lrow = (int64_t)lb * blen + off;  // local row of the chunk start
+        const int64_t grow = trow0 + lrow;               // level row of the chunk start
+        Eq2 cur;
+        if (active) {
+            cur = leaf_smem<KEEP>(s.a + lrow, s.b + lrow, s.c + lrow, s.d + lrow, len, grow, bad);
+        } else {
+            cur = Eq2{0, 1, 0, 0, 0, 1, 0, 0};
+        }
+        // ---- up the lane tree ----
+        MergeSave sv[10];
+        for (int lv = 0; lv < logg; ++lv) {
+            const int h = 1 << lv;
+            Eq2 oth;
+            if (h < 32) {
+                oth = shfl_down_eq(cur, h);
+            } else {
+                if ((c & (2 * h - 1)) == h) s.xeq[tid >> 5] = cur;
+                __syncthreads();
+                if ((c & (2 * h - 1)) == 0) oth = s.xeq[(tid + h) >> 5];
+                __syncthreads();
+            }
+            if ((c & (2 * h - 1)) == 0 && active) {
+                // row_t = last row of segment A = chunk (c+h-1)'s last row
+                const int64_t ca = c + h;  // first chunk of B
+                const int64_t offb = ca * Llo + (ca < ext ? ca : ext);
+                const int64_t row_t = trow0 + (int64_t)lb * blen + offb - 1;
+                cur = merge(cur, oth, row_t, bad, sv[lv]);
+            }
+        }
+        // ---- root ----
+        double xs = 0, xe = 0;
+        if (c == 0 && active) {
+            const int64_t jb = blk_base + b0 + lb;
+            if (MODE == kStage1) {
+                out.sub[2 * jb] = cur.a1;     out.sub[2 * jb + 1] = cur.a2;
+                out.diag[2 * jb] = cur.b1;    out.diag[2 * jb + 1] = cur.b2;
+                out.sup[2 * jb] = cur.g1;     out.sup[2 * jb + 1] = cur.g2;
+                out.rhs[2 * jb] = cur.d1;     out.rhs[2 * jb + 1] = cur.d2;
+            } else if (MODE == kStage3) {
+                xs = xi[2 * jb];
+                xe = xi[2 * jb + 1];
+            } else {  // kSolve: the whole system is this one block
+                if (blen == 1) {
+                    check_pivot(cur.b1, 0, bad);
+                    xs = xe = cur.d1 * rcp(cur.b1);
+                } else {
+                    root_solve(cur, blen - 1, bad, xs, xe);
+                }
+            }
+        }
+        if (MODE != kStage1) {
+            // ---- down the lane tree ----
+            for (int lv = logg - 1; lv >= 0; --lv) {
+                const int h = 1 << lv;
+                double xt = 0;
+                if ((c & (2 * h - 1)) == 0) xt = merge_xt(sv[lv], xs, xe);
+                double rxt, rxe;
+                if (h < 32) {
+                    rxt = __shfl_up_sync(0xffffffffu, xt, h);
+                    rxe = __shfl_up_sync(0xffffffffu, xe, h);
+                } else {
+                    if ((c & (2 * h - 1)) == 0) {
+                        s.xpass[2 * ((tid + h) >> 5)] = xt;
+                        s.xpass[2 * ((tid + h) >> 5) + 1] = xe;
+                    }
+                    __syncthreads();
+                    rxt = s.xpass[2 * (tid >> 5)];
+                    rxe = s.xpass[2 * (tid >> 5) + 1];
+                    __syncthreads();
+                }
+                if ((c & (2 * h - 1)) == h) {
+                    xs = first_from_e1(cur, rxt, rxe);
+                    xe = rxe;
+                } else if ((c & (2 * h - 1)) == 0) {
+                    xe = xt;
+                }
+            }
+            // ---- leaf expansion into the a-slots, then coalesced store ----
+            if (active) {
+                double* a = s.a + lrow;
+                const double* rb = s.b + lrow;
+                const double* g = s.c + lrow;
+                const double* dd = s.d + lrow;
+                double prev = xs;
+                for (int i = 1; i < len - 1; ++i) {
+                    const double xv = (dd[i] - a[i] * prev - g[i] * xe) * rb[i];
+                    a[i] = xv;
+                    prev = xv;
+                }
+                a[0] = xs;
+                if (len > 1) a[len - 1] = xe;
+            }
+            __syncthreads();
+            for (int64_t i = tid; i < trows; i += T) x[trow0 + i] = s.a[i];
+        }
+        __syncthreads();
+        (void)lane;
+    }
+    report_pivot(err, level, bad);
+}
+
+// ===========================================================================
+// Sharded top level: every rank holds the gathered [eq8 x P] (layout per rank:
+// sub[2], diag[2], sup[2], rhs[2]); assemble the 2P-row interface
+// (assemble_interface, partition.hpp:139-149) and solve it with Thomas
+// (tridiagonal.hpp:52-72) in one thread; keep this rank's (x_s, x_e).
+// ===========================================================================
+__global__ void k_gather_solve(const double* __restrict__ eqs, int nranks, int rank,
+                               double* __restrict__ x2, double* __restrict__ scratch,
+                               unsigned long long* err, int level) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int n = 2 * nranks;
+    double* cm = scratch;
+    double* xx = scratch + n;
+    int64_t bad = INT64_MAX;
+    for (int i = 0; i < n; ++i) {
+        const double* e = eqs + 8 * (i >> 1);
+        const int k = i & 1;
+        const double sub = e[0 + k], dg = e[2 + k], sp = e[4 + k], rh = e[6 + k];
+        if (i == 0) {
+            check_pivot(dg, 0, bad);
+            cm[0] = sp / dg;
+            xx[0] = rh / dg;
+        } else {
+            const double piv = dg - sub * cm[i - 1];
+            check_pivot(piv, i, bad);
+            cm[i] = sp / piv;
+            xx[i] = (rh - sub * xx[i - 1]) / piv;
+        }
+    }
+    for (int i = n - 2; i >= 0; --i) xx[i] -= cm[i] * xx[i + 1];
+    x2[0] = xx[2 * rank];
+    x2[1] = xx[2 * rank + 1];
+    report_pivot(err, level, bad);
+}
+
+// ===========================================================================
+// Device generator: same distributions as generate_system (bench.hpp:68-93)
+// — a,c,d ~ U[-1,1), b = delta*(|a|+|c|)+1, whole-row sign flip with p=0.5,
+// sub[0] = super[N-1] = 0 — from a counter-based hash of (seed, global row),
+// so any shard generates its slice of the same global system. NOT
+// bit-identical to std::mt19937_64; used for throughput runs only.
+// ===========================================================================
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double canon(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
+
+__global__ void k_generate(int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
+                           double* __restrict__ sub, double* __restrict__ diag,
+                           double* __restrict__ sup, double* __restrict__ rhs) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = (uint64_t)(row0 + i);
+        const uint64_t k = mix64(seed * 0x9E3779B97F4A7C15ULL + 0x632BE59BD9B4E019ULL) ^ (g * 4);
+        double a = canon(mix64(k + 0)) * 2.0 - 1.0;
+        double cc = canon(mix64(k + 1)) * 2.0 - 1.0;
+        double d = canon(mix64(k + 2)) * 2.0 - 1.0;
+        const bool fl = canon(mix64(k + 3)) < 0.5;
+        if (row0 + i == 0) a = 0.0;
+        if (row0 + i == n_global - 1) cc = 0.0;
+        double b = delta * (fabs(a) + fabs(cc)) + 1.0;
+        if (fl) { a = -a; b = -b; cc = -cc; d = -d; }
+        sub[i] = a;
+        diag[i] = b;
+        sup[i] = cc;
+        rhs[i] = d;
+    }
+}
+
+// residual_inf (tridiagonal.hpp:74-87): out[0] = max|Ax-d|, out[1] = max(1, max|d|),
+// both as order-preserving uint64 bit patterns of non-negative doubles.
+__global__ void k_residual(SysPtrs sys, int64_t n, const double* __restrict__ x,
+                           unsigned long long* out) {
+    double num = 0, den = 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double ax = sys.diag[i] * x[i];
+        if (i > 0) ax += sys.sub[i] * x[i - 1];
+        if (i + 1 < n) ax += sys.sup[i] * x[i + 1];
+        num = fmax(num, fabs(ax - sys.rhs[i]));
+        den = fmax(den, fabs(sys.rhs[i]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        num = fmax(num, __shfl_down_sync(0xffffffffu, num, o));
+        den = fmax(den, __shfl_down_sync(0xffffffffu, den, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out + 0, (unsigned long long)__double_as_longlong(num));
+        atomicMax(out + 1, (unsigned long long)__double_as_longlong(den));
+    }
+}
+
+// ===========================================================================
+// Launchers
+// ===========================================================================
+template <int L, int G, bool VEC>
+static cudaError_t launch_fast_t(int mode, const SysPtrs& sys, int64_t nblocks, const IfacePtrs& out,
+                                 const double* xi, double* x, unsigned long long* err, int level,
+                                 int grid_cap, cudaStream_t st) {
+    const int64_t nchunks = nblocks * G;
+    int64_t grid = (nchunks + kFastThreads - 1) / kFastThreads;
+    if (grid > grid_cap) grid = grid_cap;
+    if (grid < 1) grid = 1;
+    if (mode == kStage1)
+        k_fast<L, G, kStage1, VEC><<<(unsigned)grid, kFastThreads, 0, st>>>(sys, nblocks, out, xi, x, err, level);
+    else
+        k_fast<L, G, kStage3, VEC><<<(unsigned)grid, kFastThreads, 0, st>>>(sys, nblocks, out, xi, x, err, level);
+    return cudaGetLastError();
+}
+
+template <int L, int G>
+static cudaError_t launch_fast_v(bool vec, int mode, const SysPtrs& sys, int64_t nblocks,
+                                 const IfacePtrs& out, const double* xi, double* x,
+                                 unsigned long long* err, int level, int grid_cap, cudaStream_t st) {
+    if (vec) return launch_fast_t<L, G, true>(mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
+    return launch_fast_t<L, G, false>(mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
+}
+
+bool fast_shape(int64_t m, int* L, int* G) {
+    switch (m) {
+        case 4: *L = 4; *G = 1; return true;
+        case 5: *L = 5; *G = 1; return true;
+        case 8: *L = 8; *G = 1; return true;
+        case 10: *L = 5; *G = 2; return true;
+        case 16: *L = 8; *G = 2; return true;
+        case 20: *L = 5; *G = 4; return true;
+        case 32: *L = 8; *G = 4; return true;
+        case 40: *L = 5; *G = 8; return true;
+        case 64: *L = 8; *G = 8; return true;
+        case 80: *L = 5; *G = 16; return true;
+        case 128: *L = 8; *G = 16; return true;
+        case 160: *L = 5; *G = 32; return true;
+        case 256: *L = 8; *G = 32; return true;
+        default: return false;
+    }
+}
+
+cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs& sys, int64_t nblocks,
+                        const IfacePtrs& out, const double* xi, double* x, unsigned long long* err,
+                        int level, int grid_cap, cudaStream_t st) {
+#define TPB_CASE(MM, LL, GG) \
+    case MM: return launch_fast_v<LL, GG>(vec, mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
+    switch (m) {
+        TPB_CASE(4, 4, 1)
+        TPB_CASE(5, 5, 1)
+        TPB_CASE(8, 8, 1)
+        TPB_CASE(10, 5, 2)
+        TPB_CASE(16, 8, 2)
+        TPB_CASE(20, 5, 4)
+        TPB_CASE(32, 8, 4)
+        TPB_CASE(40, 5, 8)
+        TPB_CASE(64, 8, 8)
+        TPB_CASE(80, 5, 16)
+        TPB_CASE(128, 8, 16)
+        TPB_CASE(160, 5, 32)
+        TPB_CASE(256, 8, 32)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TPB_CASE
+}
+
+size_t generic_smem_bytes(int threads, int G, int64_t blen) {
+    const int64_t bpc = threads / G;
+    return (size_t)(4 * bpc * blen) * sizeof(double) + (size_t)((threads + 31) / 32) * sizeof(Eq2) +
+           (size_t)(2 * ((threads + 31) / 32)) * sizeof(double);
+}
+
+cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs& sys, int64_t row_base,
+                           int64_t blk_base, int64_t nblocks, int64_t blen, const IfacePtrs& out,
+                           const double* xi, double* x, unsigned long long* err, int level,
+                           cudaStream_t st) {
+    const size_t smem = generic_smem_bytes(threads, G, blen);
+    if (smem > kMaxDynSmem) return cudaErrorInvalidValue;
+    if (mode == kStage1) {
+        k_generic<kStage1><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
+    } else if (mode == kStage3) {
+        k_generic<kStage3><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
+    } else {
+        k_generic<kSolve><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t init_kernel_attributes() {
+    cudaError_t e = cudaFuncSetAttribute(k_generic<kStage1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_generic<kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_generic<kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+    return e;
+}
+
+cudaError_t launch_gather_solve(const double* eqs, int nranks, int rank, double* x2, double* scratch,
+                                unsigned long long* err, int level, cudaStream_t st) {
+    k_gather_solve<<<1, 32, 0, st>>>(eqs, nranks, rank, x2, scratch, err, level);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_generate(int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
+                            double* sub, double* diag, double* sup, double* rhs, int sms,
+                            cudaStream_t st) {
+    int64_t grid = (n + 255) / 256;
+    if (grid > (int64_t)sms * 16) grid = (int64_t)sms * 16;
+    if (grid < 1) grid = 1;
+    k_generate<<<(unsigned)grid, 256, 0, st>>>(n, row0, n_global, seed, delta, sub, diag, sup, rhs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual(const SysPtrs& sys, int64_t n, const double* x, unsigned long long* out,
+                            int sms, cudaStream_t st) {
+    int64_t grid = (n + 255) / 256;
+    if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
+    if (grid < 1) grid = 1;
+    k_residual<<<(unsigned)grid, 256, 0, st>>>(sys, n, x, out);
+    return cudaGetLastError();
+}
+
+int fast_max_active_blocks(int64_t m, bool vec, int mode) {
+    int L, G, nb = 0;
+    if (!fast_shape(m, &L, &G)) return 0;
+#define TPB_OCC(MM, LL, GG)                                                                          \
+    case MM:                                                                                         \
+        if (mode == kStage1) {                                                                       \
+            if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast<LL, GG, kStage1, true>, kFastThreads, 0); \
+            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast<LL, GG, kStage1, false>, kFastThreads, 0); \
+        } else {                                                                                     \
+            if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast<LL, GG, kStage3, true>, kFastThreads, 0); \
+            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast<LL, GG, kStage3, false>, kFastThreads, 0); \
+        }                                                                                            \
+        break;
+    switch (m) {
+        TPB_OCC(4, 4, 1)
+        TPB_OCC(5, 5, 1)
+        TPB_OCC(8, 8, 1)
+        TPB_OCC(10, 5, 2)
+        TPB_OCC(16, 8, 2)
+        TPB_OCC(20, 5, 4)
+        TPB_OCC(32, 8, 4)
+        TPB_OCC(40, 5, 8)
+        TPB_OCC(64, 8, 8)
+        TPB_OCC(80, 5, 16)
+        TPB_OCC(128, 8, 16)
+        TPB_OCC(160, 5, 32)
+        TPB_OCC(256, 8, 32)
+        default: break;
+    }
+#undef TPB_OCC
+    return nb;
+}
+
+}  // namespace tpb

@@ -1,0 +1,54 @@
+// Internal launcher interface between the C-ABI layer and the sm_100a kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tpb {
+
+constexpr int kStage1 = 0;  // reduce blocks -> next level's interface rows
+constexpr int kStage3 = 1;  // expand blocks from the next level's solution
+constexpr int kSolve = 2;   // whole system as one block: reduce, 2x2 root, expand
+
+constexpr int kFastThreads = 256;
+constexpr int kGenericThreads = 256;
+constexpr int kFinalThreads = 1024;
+// Largest system the single-CTA finishing solve keeps in shared memory
+// (32 B per row; 6144 rows = 192 KiB of the 227 KiB opt-in limit).
+constexpr int64_t kFinalCap = 6144;
+constexpr size_t kMaxDynSmem = 227 * 1024;
+constexpr unsigned long long kNoError = ~0ULL;
+
+struct SysPtrs {
+    const double* sub;
+    const double* diag;
+    const double* sup;
+    const double* rhs;
+};
+struct IfacePtrs {
+    double* sub;
+    double* diag;
+    double* sup;
+    double* rhs;
+};
+
+cudaError_t init_kernel_attributes();
+bool fast_shape(int64_t m, int* L, int* G);
+int fast_max_active_blocks(int64_t m, bool vec, int mode);
+cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs& sys, int64_t nblocks,
+                        const IfacePtrs& out, const double* xi, double* x, unsigned long long* err,
+                        int level, int grid_cap, cudaStream_t st);
+size_t generic_smem_bytes(int threads, int G, int64_t blen);
+cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs& sys, int64_t row_base,
+                           int64_t blk_base, int64_t nblocks, int64_t blen, const IfacePtrs& out,
+                           const double* xi, double* x, unsigned long long* err, int level,
+                           cudaStream_t st);
+cudaError_t launch_gather_solve(const double* eqs, int nranks, int rank, double* x2, double* scratch,
+                                unsigned long long* err, int level, cudaStream_t st);
+cudaError_t launch_generate(int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
+                            double* sub, double* diag, double* sup, double* rhs, int sms,
+                            cudaStream_t st);
+cudaError_t launch_residual(const SysPtrs& sys, int64_t n, const double* x, unsigned long long* out,
+                            int sms, cudaStream_t st);
+
+}  // namespace tpb

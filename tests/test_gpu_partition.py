@@ -1,0 +1,268 @@
+"""GPU parity: the sm_100a partition solve (through the C-ABI) against the CPU
+oracle on identical inputs. Mirrors the reference's own tests
+(proj/tests/test_partition.cpp, test_tridiagonal.cpp, acceptance.cpp
+criteria 1-2) plus the BASELINE configs.
+
+Parity gates:
+  rel_inf_diff(x, x_oracle)                    <= 1e-10   (oracles.hpp:46-53)
+  max |dx_i| / max(|x_oracle_i|, 1e-6)         <= 1e-10   (floored elementwise)
+  residual_inf(sys, x)                         <= 1e-12   (tridiagonal.hpp:74-87)
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_NORM = 1e-10
+TOL_FLOOR = 1e-10
+TOL_RES = 1e-12
+
+
+def _sys(tp, s):
+    return tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs)
+
+
+def _check(oracle_mod, s, x, ref, tol=TOL_NORM):
+    assert np.all(np.isfinite(x))
+    d = oracle_mod.rel_inf_diff(x, ref)
+    f = oracle_mod.floored_rel_diff(x, ref)
+    r = oracle_mod.residual_inf(s, x)
+    assert d <= tol, f"rel_inf_diff {d}"
+    assert f <= max(tol, TOL_FLOOR), f"floored elementwise {f}"
+    assert r <= TOL_RES, f"residual {r}"
+
+
+# ---------------------------------------------------------------- BASELINE configs
+def test_config1_n1e4_m4(tp, oracle_mod):
+    s = oracle_mod.generate_system(10_000, 1)
+    ref = oracle_mod.solve_partition(s, [4])
+    x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([4]))
+    _check(oracle_mod, s, x, ref)
+    # SURVEY §8(c) golden pins (tolerance-checked)
+    assert abs(x[0] - -0.271138473871889) <= 1e-12
+    assert abs(x[5000] - 0.40220197517592371) <= 1e-12
+    assert abs(x[9999] - 0.064275487179797086) <= 1e-12
+
+
+def test_config2_n1e6_knn(tp, oracle_mod):
+    pol = tp.predicted_policy(1_000_000)
+    assert pol.sizes == [32]
+    s = oracle_mod.generate_system(1_000_000, 1)
+    ref = oracle_mod.solve_partition(s, pol.sizes)
+    x = tp.solve_partition(_sys(tp, s), pol)
+    _check(oracle_mod, s, x, ref)
+    assert abs(x[500000] - 0.13624622554175128) <= 1e-12
+    assert abs(x[-1] - 0.48663996410395077) <= 1e-12
+
+
+def test_config3_n1e8_recursive(tp, oracle_mod):
+    pol = tp.predicted_policy(100_000_000)
+    assert pol.sizes == [64, 10, 32, 16]
+    s = oracle_mod.generate_system(100_000_000, 1)
+    ref = oracle_mod.solve_partition(s, pol.sizes)
+    x = tp.solve_partition(_sys(tp, s), pol)
+    # normwise + floored elementwise + residual (plain elementwise 1e-10 fails
+    # even between the reference's own solvers at this size)
+    _check(oracle_mod, s, x, ref)
+    assert abs(x[50_000_000] - -0.28797162068321597) <= 1e-12
+    assert abs(x[-1] - 0.12850268247978247) <= 1e-12
+
+
+# ------------------------------------------------------------ test_partition.cpp
+def test_identity_system_any_policy(tp):
+    n = 100
+    sys = tp.TridiagonalSystem(np.zeros(n), np.ones(n), np.zeros(n), np.arange(n) - 50.0)
+    x = tp.solve_partition(sys, tp.RecursionPolicy([8, 10, 4]))
+    assert np.array_equal(x, sys.rhs)
+
+
+def test_n16_m4_dense(tp, oracle_mod):
+    s = oracle_mod.generate_system(16, 3)
+    x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([4]))
+    assert oracle_mod.rel_inf_diff(x, oracle_mod.dense_solve(s)) <= 1e-10
+
+
+def test_n1e4_depths_agree_with_thomas(tp, oracle_mod):
+    s = oracle_mod.generate_system(10_000, 17)
+    ref = oracle_mod.thomas_solve(s)
+    x0 = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([8]))
+    x2 = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([8, 10, 8]))
+    assert oracle_mod.rel_inf_diff(x0, ref) <= 1e-10
+    assert oracle_mod.rel_inf_diff(x2, ref) <= 1e-10
+    assert oracle_mod.rel_inf_diff(x0, x2) <= 1e-10
+
+
+def test_depths_0_to_4(tp, oracle_mod):
+    s = oracle_mod.generate_system(20_000, 23)
+    ref = oracle_mod.thomas_solve(s)
+    for depth in range(5):
+        sizes = [10 if l % 2 else 8 for l in range(depth + 1)]
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes))
+        assert oracle_mod.rel_inf_diff(x, ref) <= 1e-9
+
+
+def test_tiny_systems_fall_back(tp, oracle_mod):
+    for n in (1, 2, 3):
+        s = oracle_mod.generate_system(max(n, 2), 2) if n > 1 else None
+        if n == 1:
+            sys = tp.TridiagonalSystem([0.0], [2.0], [0.0], [3.0])
+            x = tp.solve_partition(sys, tp.RecursionPolicy([4]))
+            assert x[0] == 1.5
+            continue
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([4]))
+        assert oracle_mod.residual_inf(s, x) <= 1e-12
+
+
+def test_thomas_drop_in(tp, oracle_mod):
+    for n in (2, 50, 5000, 7000, 100_000):
+        s = oracle_mod.generate_system(n, 7)
+        x = tp.thomas_solve(_sys(tp, s))
+        ref = oracle_mod.thomas_solve(s)
+        assert oracle_mod.rel_inf_diff(x, ref) <= 1e-10
+        assert oracle_mod.residual_inf(s, x) <= 1e-12
+
+
+def test_thomas_hand_checked_2x2(tp):
+    sys = tp.TridiagonalSystem([0, 1], [2, 2], [1, 0], [3, 3])
+    x = tp.thomas_solve(sys)
+    assert abs(x[0] - 1) <= 1e-14 and abs(x[1] - 1) <= 1e-14
+
+
+# ------------------------------------------------- acceptance.cpp criteria 1 and 2
+def test_criterion1_200_random_systems(tp, oracle_mod):
+    """acceptance.cpp:72-100: n in [10, 1e5], m in {2,4,7,8,16,20,32,40,64}, R in 0..4."""
+    rng = np.random.default_rng(20240601)
+    m_choices = [2, 4, 7, 8, 16, 20, 32, 40, 64]
+    for _ in range(200):
+        n = int(rng.integers(10, 100_001))
+        depth = int(rng.integers(0, 5))
+        sizes = [int(m_choices[rng.integers(0, len(m_choices))]) for _ in range(depth + 1)]
+        s = oracle_mod.generate_system(n, int(rng.integers(0, 2**63)))
+        ref = oracle_mod.thomas_solve(s)
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes))
+        d = oracle_mod.rel_inf_diff(x, ref)
+        assert d <= 1e-10, f"n={n} sizes={sizes} diff={d}"
+
+
+def test_criterion2_interface_dominance_and_parity(tp, oracle_mod):
+    """acceptance.cpp:102-123 via the observer overload; also compares every
+    device interface level with the oracle's assemble_interface output."""
+    rng = np.random.default_rng(7)
+    for _ in range(100):
+        n = int(rng.integers(10, 2010))
+        depth = int(rng.integers(0, 3))
+        sizes = [int(rng.integers(2, 17)) for _ in range(depth + 1)]
+        s = oracle_mod.generate_system(n, int(rng.integers(0, 2**63)))
+        dev_levels, ref_levels = [], []
+        tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes),
+                           lambda f, lvl: dev_levels.append((lvl, f)))
+        oracle_mod.solve_partition(s, sizes, observer=lambda l, a, b, c, d: ref_levels.append((l, a, b, c, d)))
+        assert [l for l, _ in dev_levels] == [l for l, *_ in ref_levels]
+        for (lvl, f), (_, a, b, c, d) in zip(dev_levels, ref_levels):
+            assert np.all(np.abs(f.diag) >= np.abs(f.sub) + np.abs(f.super) - 1e-12)
+            for got, want in ((f.sub, a), (f.diag, b), (f.super, c), (f.rhs, d)):
+                scale = max(1.0, float(np.max(np.abs(want))))
+                assert float(np.max(np.abs(got - want))) / scale <= 1e-12
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 7, 8, 10, 13, 16, 20, 31, 32, 33, 40, 64, 65, 100, 128,
+                               250, 256, 500, 625, 1000, 1250])
+def test_every_block_size(tp, oracle_mod, m):
+    """Fast shapes and the generic path, with tail blocks of every kind."""
+    for n in (m + 1, 3 * m, 3 * m + 1, 3 * m + 2, 50_003):
+        if n < 4:
+            continue
+        s = oracle_mod.generate_system(n, 1000 + m)
+        ref = oracle_mod.solve_partition(s, [m])
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([m]))
+        _check(oracle_mod, s, x, ref)
+
+
+def test_m_at_least_n(tp, oracle_mod):
+    for n, m in ((5, 8), (64, 64), (63, 64), (100, 5000)):
+        s = oracle_mod.generate_system(n, 4)
+        ref = oracle_mod.solve_partition(s, [m])
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([m]))
+        _check(oracle_mod, s, x, ref)
+
+
+def test_large_final_system_uses_internal_levels(tp, oracle_mod):
+    # R=0 with m=4 at N=1e5 leaves a 50,000-row final system
+    s = oracle_mod.generate_system(100_000, 9)
+    ref = oracle_mod.solve_partition(s, [4])
+    x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([4]))
+    _check(oracle_mod, s, x, ref)
+
+
+def test_sub0_and_super_last_are_ignored(tp, oracle_mod):
+    s = oracle_mod.generate_system(5000, 11)
+    ref = oracle_mod.solve_partition(s, [16])
+    sub, sup = s.sub.copy(), s.sup.copy()
+    sub[0], sup[-1] = 123.0, -77.0
+    x = tp.solve_partition(tp.TridiagonalSystem(sub, s.diag, sup, s.rhs), tp.RecursionPolicy([16]))
+    _check(oracle_mod, s, x, ref)
+
+
+def test_invalid_policy_and_empty_system(tp):
+    sys = tp.TridiagonalSystem([0.0, 1.0], [2.0, 2.0], [1.0, 0.0], [1.0, 1.0])
+    with pytest.raises(tp.InvalidSizeError):
+        tp.solve_partition(sys, tp.RecursionPolicy([]))
+    with pytest.raises(tp.InvalidSizeError):
+        tp.solve_partition(sys, tp.RecursionPolicy([4, 1]))
+    empty = tp.TridiagonalSystem([], [], [], [])
+    with pytest.raises(tp.InvalidSizeError):
+        tp.solve_partition(empty, tp.RecursionPolicy([4]))
+
+
+def test_zero_pivot_is_reported(tp):
+    # thomas_solve's zero-pivot case (test_tridiagonal.cpp "thomas reports a zero pivot")
+    sys = tp.TridiagonalSystem([0, 1], [0, 2], [1, 0], [1, 1])
+    with pytest.raises(tp.ZeroPivotError):
+        tp.thomas_solve(sys)
+    # a zero row inside a large system: the reference aborts (std::terminate) at
+    # K >= 128; the device solver raises ZeroPivotError instead
+    n = 4096
+    sub, diag, sup, rhs = np.zeros(n), np.ones(n), np.zeros(n), np.ones(n)
+    diag[1000] = 0.0
+    with pytest.raises(tp.ZeroPivotError):
+        tp.solve_partition(tp.TridiagonalSystem(sub, diag, sup, rhs), tp.RecursionPolicy([8]))
+
+
+def test_device_tensor_path_and_generator(tp, oracle_mod):
+    import torch
+
+    sys = tp.generate_system(2_000_003, 5, device=True)
+    assert sys.strictly_dominant()
+    pol = tp.predicted_policy(sys.size())
+    x = tp.solve_partition(sys, pol)
+    assert tp.residual_inf(sys, x) <= TOL_RES
+    host = oracle_mod.System(*(t.cpu().numpy() for t in (sys.sub, sys.diag, sys.super, sys.rhs)))
+    ref = oracle_mod.solve_partition(host, pol.sizes)
+    _check(oracle_mod, host, x.cpu().numpy(), ref)
+    # generator: sub[0] = super[-1] = 0, rows negated as a whole, |b| >= 1.5(|a|+|c|)+1
+    assert float(sys.sub[0]) == 0.0 and float(sys.super[-1]) == 0.0
+    margin = sys.diag.abs() - 1.5 * (sys.sub.abs() + sys.super.abs())
+    assert torch.allclose(margin, torch.ones_like(margin))
+
+
+def test_graph_cache_reuse_is_deterministic(tp, oracle_mod):
+    s = oracle_mod.generate_system(300_000, 3)
+    sys = _sys(tp, s)
+    xs = [tp.solve_partition(sys, tp.RecursionPolicy([32, 10, 16])) for _ in range(3)]
+    assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[1], xs[2])
+
+
+def test_sharded_solve_on_one_gpu(tp, oracle_mod):
+    """The multi-GPU algorithm with P simulated ranks on one device: each shard
+    is reduced to its boundary pair, the 8P doubles are gathered on the host,
+    and every shard solves the 2P top system redundantly and expands."""
+    import torch
+    from paper_2510_27351_b200 import sharded
+
+    n = 1_000_003
+    s = oracle_mod.generate_system(n, 13)
+    ref = oracle_mod.solve_partition(s, [32])
+    for P in (1, 2, 3, 8):
+        x = sharded.simulate_ranks(s.sub, s.diag, s.sup, s.rhs, P)
+        _check(oracle_mod, s, x, ref)
