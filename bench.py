@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 recursive partition solve on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n N_PER_GPU] [--impl ours|reference]
+
+A step is one full solve (all levels, finishing solve, Stage 3) of an
+N = 1e8-unknown strictly dominant system per GPU with the kNN-predicted
+policy [64, 10, 32, 16] (config 3). Inputs are generated on the device with
+the generate_system distributions and stay resident in HBM (3.2 GB per GPU,
+25x the 126 MB L2, so no L2 flush is needed between steps). N > 1: one
+process per GPU (torchrun), contiguous row shards of the global system
+N_global = N x 1e8 (weak scaling), one NCCL all-gather of 8 doubles per rank
+per solve, device time = max over ranks.
+
+`--impl reference` times the reference's own CPU solver (oracle/_ref: the
+unmodified reference headers, all host threads) on rank 0 only.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 unknowns/s and HBM GB/s (% roofline) at N=1e8, 1/2/4/8 B200 vs CPU ref"
+UNIT = "unknowns/s"
+ALG_BYTES_PER_UNKNOWN = 40.0   # read sub/diag/super/rhs once + write x once
+TWO_PASS_BYTES_PER_UNKNOWN = 72.0  # compulsory for an exact two-pass solve once 32N >> L2
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--n", type=float, default=1e8, help="unknowns per GPU")
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-runs", type=int, default=3)
+    p.add_argument("--prewarm", type=float, default=0.3, help="seconds of untimed solves before warm-up")
+    return p.parse_args()
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sync_boost",
+               0x40: "sw_thermal_slowdown", 0x80: "hw_thermal_slowdown",
+               0x100: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop_flag = [], set(), False
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_flag:
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_flag = True
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ reference arm
+def cpu_reference(n, runs, seed=1):
+    """The reference's solve_partition (oracle/_ref, reference headers, all
+    host threads) with the reference's own policy for N; median of `runs`
+    after 1 warm-up (bench.hpp:104-127 statistic, residual outside timing)."""
+    import numpy as np
+
+    import oracle
+
+    lib = oracle.ref()
+    sizes = np.zeros(8, dtype=np.int64)
+    depth = int(lib.ref_predict_depth(n))
+    cnt = lib.ref_recursion_sizes(n, depth, sizes.ctypes.data_as(oracle._I64))
+    sizes = sizes[:cnt].copy()
+    h = lib.ref_system_generate(n, seed)
+    x = np.empty(n)
+    try:
+        st = lib.ref_system_solve(h, sizes.ctypes.data_as(oracle._I64), len(sizes), x.ctypes.data_as(oracle._D))
+        assert st == -1, st
+        res = lib.ref_system_residual(h, x.ctypes.data_as(oracle._D))
+        times = []
+        for _ in range(runs):
+            t0 = time.perf_counter()
+            lib.ref_system_solve(h, sizes.ctypes.data_as(oracle._I64), len(sizes), None)
+            times.append(time.perf_counter() - t0)
+    finally:
+        lib.ref_system_free(h)
+    med = statistics.median(times)
+    return {"value": n / med, "unit": UNIT, "cores": int(lib.ref_hardware_concurrency()),
+            "kind": "reference", "median_s": med, "residual": res, "policy": [int(v) for v in sizes],
+            "sample": f"N={n:.0e} generate_system(seed={seed}), policy {[int(v) for v in sizes]}, "
+                      f"1 warm-up + {runs} runs, median, residual check outside timing"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    n = int(args.n)
+    # bound the run: ~3 s per N=1e8 solve on 16 cores; keep the whole run ~<= 3 min
+    budget_s = 150.0
+    per = 3.5 * n / 1e8
+    if (args.steps + args.warmup + 1) * per > budget_s:
+        n = int(max(1e6, n * budget_s / ((args.steps + args.warmup + 1) * per)))
+    import numpy as np
+
+    import oracle
+
+    lib = oracle.ref()
+    sizes = np.zeros(8, dtype=np.int64)
+    cnt = lib.ref_recursion_sizes(n, int(lib.ref_predict_depth(n)), sizes.ctypes.data_as(oracle._I64))
+    sizes = sizes[:cnt].copy()
+    h = lib.ref_system_generate(n, args.seed)
+    try:
+        for _ in range(args.warmup):
+            lib.ref_system_solve(h, sizes.ctypes.data_as(oracle._I64), len(sizes), None)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            lib.ref_system_solve(h, sizes.ctypes.data_as(oracle._I64), len(sizes), None)
+        dt = time.perf_counter() - t0
+    finally:
+        lib.ref_system_free(h)
+    value = n * args.steps / dt
+    cores = int(lib.ref_hardware_concurrency())
+    sample = (f"N={n} per step (generate_system seed={args.seed}), reference policy "
+              f"{[int(v) for v in sizes]}, {args.warmup} warm-up + {args.steps} timed solves")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "reference CPU solve_partition (oracle/_ref, reference headers)",
+                   "n_per_step": n, "policy": [int(v) for v in sizes], "threads": cores},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2510_27351_b200 as tp
+    from paper_2510_27351_b200 import sharded
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n_per = int(args.n)
+    n_glob = n_per * world
+    policy = tp.predicted_policy(n_glob)
+    lo, n_loc = sharded.shard_bounds(n_glob, world, rank)
+    stream = torch.cuda.current_stream()
+    ctx = tp.context(local)
+
+    sys_d = tp.generate_system(n_loc, args.seed, device=True, row0=lo, n_global=n_glob)
+    x = torch.empty(n_loc, dtype=torch.float64, device="cuda")
+    sys4 = [sys_d.sub, sys_d.diag, sys_d.super, sys_d.rhs]
+
+    if world == 1:
+        def step():
+            tp.solve_partition_async(sys_d, policy, out=x)
+    else:
+        solver = sharded.ShardedSolver()
+
+        def step():
+            solver.solve(sys4, n_glob, policy, out=x)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # untimed: graph capture + clock ramp (~0.3 s of solves), then W warm-up steps
+    step()
+    barrier()
+    t_end = time.perf_counter() + args.prewarm
+    while time.perf_counter() < t_end:
+        step()
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches_per_step = ctx.last_launch_count()
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        if world > 1:
+            launches_per_step += 0  # the all-gather is NCCL's, not counted as ours
+    ms_step = ms / args.steps
+    value = n_glob * args.steps / (ms / 1e3)
+
+    # correctness of what was timed
+    tp.check_device_error()
+    res = tp.residual_inf(sys_d, x) if world == 1 else None
+    if world > 1:
+        # residual of the local rows (shard-boundary rows need neighbours; skip them)
+        res = tp.residual_inf(tp.TridiagonalSystem(*(t[1:-1] for t in sys4)), x[1:-1]) if n_loc > 2 else 0.0
+
+    # per-kernel durations (CUDA events on the launch stream, same inputs)
+    prof = {}
+    if world == 1:
+        import ctypes as C
+        from paper_2510_27351_b200._lib import TpError, lib
+        sz = np.asarray(policy.sizes, dtype=np.int64)
+        reps = 10
+        for _ in range(reps if args.prewarm > 0 else 1):
+            kms = (C.c_float * 64)()
+            names = C.create_string_buffer(64 * 32)
+            nk = C.c_int32()
+            err = TpError()
+            tp.context().set_stream(tp.torch_stream())
+            st = lib.tp_solve_profile_f64_dev(ctx.handle, *sys_d._dev_ptrs(), n_loc,
+                                              sz.ctypes.data_as(C.POINTER(C.c_int64)), len(sz),
+                                              C.c_void_p(x.data_ptr()), kms, names, 64, C.byref(nk),
+                                              C.byref(err))
+            if st != 0:
+                raise RuntimeError(err.msg.decode())
+            for i in range(nk.value):
+                nm = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
+                prof.setdefault(nm, []).append(kms[i])
+        prof = {k: statistics.median(v) for k, v in prof.items()}
+
+    # end to end through the public API: pinned host buffers, H2D + solve + D2H
+    e2e = None
+    h2d = 4 * 8 * n_loc
+    d2h = 8 * n_loc
+    if args.e2e_steps > 0:
+        host = [t.cpu().pin_memory() for t in sys4]
+        hx = torch.empty(n_loc, dtype=torch.float64).pin_memory()
+        if world == 1:
+            hs = tp.TridiagonalSystem(*(t.numpy() for t in host))
+            xo = hx.numpy()
+            import ctypes as C
+            from paper_2510_27351_b200._lib import lib
+            sz = np.asarray(policy.sizes, dtype=np.int64)
+            tp.context().set_stream(tp.torch_stream())
+
+            def e2e_step():
+                from paper_2510_27351_b200.tridpart import _call
+                _call(lib.tp_solve_partition_f64, ctx.handle, *hs._host_ptrs(), n_loc,
+                      sz.ctypes.data_as(C.POINTER(C.c_int64)), len(sz), C.c_void_p(xo.ctypes.data))
+        else:
+            dsys = [torch.empty_like(t) for t in sys4]
+            solver = sharded.ShardedSolver()
+
+            def e2e_step():
+                for d, h in zip(dsys, host):
+                    d.copy_(h, non_blocking=True)
+                solver.solve(dsys, n_glob, policy, out=x)
+                hx.copy_(x, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": n_glob * args.e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+               "ms_per_step": dt / args.e2e_steps * 1e3,
+               "path": "tp_solve_partition_f64 (C-ABI host-pointer entry of solve_partition), pinned host buffers"
+               if world == 1 else "pinned host -> device copy, ShardedSolver.solve, device -> pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference(n_per, args.cpu_runs, args.seed)
+        except Exception as e:  # reference build missing on this box
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        peak, peak_src = hbm_peak()
+        roof = None
+        if prof:
+            k = "stage3:L0"
+            t_k = prof.get(k)
+            achieved = ALG_BYTES_PER_UNKNOWN * n_loc / (t_k * 1e-3) / 1e9
+            traffic = None
+            summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
+            if os.path.exists(summ):
+                try:
+                    with open(summ) as f:
+                        traffic = json.load(f).get("stage3_L0", {}).get("dram_bytes")
+                except Exception:
+                    traffic = None
+            roof = {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "alg_bytes_per_launch": ALG_BYTES_PER_UNKNOWN * n_loc,
+                    "kernel_ms": t_k, "peak_source": peak_src,
+                    "kernel_share_of_step": t_k / sum(prof.values())}
+        solve_gbs = ALG_BYTES_PER_UNKNOWN * n_glob / (ms_step * 1e-3) / 1e9 / world
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: device counter-based generator with generate_system's distributions",
+            "config": {"workload": "recursive partition solve, kNN policy, N=1e8 per GPU (config 3)",
+                       "n_per_gpu": n_per, "n_global": n_glob, "policy": policy.sizes,
+                       "l2": "inputs 3.2 GB/GPU >> 126 MB L2 (no flush)",
+                       "parallelism": "single GPU" if world == 1 else f"{world} contiguous shards + NCCL all-gather"},
+            "hbm": {"solve_GBps_40B_per_gpu": solve_gbs,
+                    "frac_40B": solve_gbs / peak,
+                    "frac_72B": solve_gbs * TWO_PASS_BYTES_PER_UNKNOWN / ALG_BYTES_PER_UNKNOWN / peak,
+                    "peak_GBps": peak, "peak_source": peak_src},
+            "roofline": roof,
+            "kernels_ms": prof or None,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches_per_step * args.steps),
+            "launches_per_step": int(launches_per_step),
+            "clocks": clk.summary(),
+            "residual": res,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

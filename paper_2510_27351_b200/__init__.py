@@ -8,6 +8,6 @@ from .tridpart import (  # noqa: F401
     default_depth_model, default_size_model, fit_depth_model, fit_knn, generate_system,
     kMaxRecursionDepth, kModelFormatVersion, kPivotFloor, load_model, make_plan, plan_levels,
     predict, predicted_policy, read_observations, recursion_sizes, residual_inf, save_model,
-    solve_partition, solve_partition_async, thomas_solve)
+    solve_partition, solve_partition_async, thomas_solve, torch_stream)
 
 __version__ = "0.1.0"

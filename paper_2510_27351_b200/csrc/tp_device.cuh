@@ -39,14 +39,34 @@ struct MergeSave {
     double d1, g1, r1, a2;
 };
 
-// Correctly rounded FP64 reciprocal; w = c * rcp(p) replaces the reference's
-// c / p (<= 1 ulp apart).
-__device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
-
-// Zero-pivot bookkeeping: remember the smallest offending row of this thread.
-__device__ __forceinline__ void check_pivot(double p, int64_t row, int64_t& bad) {
-    if (fabs(p) < kPivotFloor) bad = (row < bad) ? row : bad;
+// FP64 reciprocal: MUFU.RCP64H seed + two Newton steps (error ~1 ulp); no
+// slow path, because every pivot it sees passed the |p| >= 1e-30 floor check
+// (or is already reported as a zero pivot). w = c * rcp(p) replaces the
+// reference's c / p (<= ~2 ulp apart; parity is by tolerance).
+__device__ __forceinline__ double rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
 }
+
+// Zero-pivot bookkeeping (|pivot| < kPivotFloor -> ZeroPivotError).
+// RowGuard remembers the smallest offending row (generic / finishing paths);
+// MinGuard keeps only min|pivot| (one DMNMX per pivot on the hot path) and the
+// caller reports the chunk's first row when it fell below the floor.
+struct RowGuard {
+    int64_t bad = INT64_MAX;
+    __device__ __forceinline__ void see(double p, int64_t row) {
+        if (fabs(p) < kPivotFloor) bad = (row < bad) ? row : bad;
+    }
+};
+struct MinGuard {
+    double pmin = 1.0e300;
+    __device__ __forceinline__ void see(double p, int64_t) { pmin = fmin(pmin, fabs(p)); }
+    __device__ __forceinline__ bool tripped() const { return pmin < kPivotFloor; }
+};
 
 // err word encodes (level << 48) | row; atomicMin keeps the lexicographically
 // first failure. Reported to the host as ZeroPivotError(row) at `level`.
@@ -69,8 +89,8 @@ struct Chunk {
 };
 
 // Stage-1 leaf: E1/E2 only (no per-row storage).
-template <int L>
-__device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int len, int64_t row0, int64_t& bad) {
+template <int L, class G>
+__device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int len, int64_t row0, G& bad) {
     Eq2 q;
     // up-sweep: seed row len-2, run i = len-3 .. 0
     double beta = 0, gamma = 0, delta = 0;
@@ -81,7 +101,7 @@ __device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int len, int64_t r
             gamma = r.c[i];
             delta = r.d[i];
         } else if (i < len - 2) {
-            check_pivot(beta, row0 + i + 1, bad);
+            bad.see(beta, row0 + i + 1);
             const double w = r.c[i] * rcp(beta);
             beta = r.b[i] - w * r.a[i + 1];
             gamma = -w * gamma;
@@ -98,7 +118,7 @@ __device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int len, int64_t r
 #pragma unroll
     for (int i = 2; i < L; ++i) {
         if (i < len) {
-            check_pivot(bp, row0 + i - 1, bad);
+            bad.see(bp, row0 + i - 1);
             const double w = r.a[i] * rcp(bp);
             phi = -w * phi;
             bp = r.b[i] - w * r.c[i - 1];
@@ -115,9 +135,9 @@ __device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int len, int64_t r
 
 // Stage-3 leaf: same sweeps, but keeps rcp(beta_i), gamma_i, delta_i of the
 // interior rows for back_substitute (partition.hpp:156-172).
-template <int L>
+template <int L, class G>
 __device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int len, int64_t row0,
-                                                int64_t& bad, double (&rbeta)[L],
+                                                G& bad, double (&rbeta)[L],
                                                 double (&gam)[L], double (&del)[L]) {
     Eq2 q;
     double beta = 0, gamma = 0, delta = 0;
@@ -128,7 +148,7 @@ __device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int len, int6
             gamma = r.c[i];
             delta = r.d[i];
         } else if (i < len - 2) {
-            check_pivot(beta, row0 + i + 1, bad);
+            bad.see(beta, row0 + i + 1);
             const double rb = rcp(beta);
             rbeta[i + 1] = rb;
             const double w = r.c[i] * rb;
@@ -148,7 +168,7 @@ __device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int len, int6
 #pragma unroll
     for (int i = 2; i < L; ++i) {
         if (i < len) {
-            check_pivot(bp, row0 + i - 1, bad);
+            bad.see(bp, row0 + i - 1);
             const double w = r.a[i] * rcp(bp);
             phi = -w * phi;
             bp = r.b[i] - w * r.c[i - 1];
@@ -186,16 +206,17 @@ __device__ __forceinline__ void leaf_expand(const Chunk<L>& r, int len, const do
 // Merge of adjacent segments A=[s,t], B=[t+1,e]: reduce_block on the 4-row
 // system [A.E1, A.E2, B.E1, B.E2] in the unknowns (x_s, x_t, x_{t+1}, x_e).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ Eq2 merge(const Eq2& A, const Eq2& B, int64_t row_t, int64_t& bad,
+template <class G>
+__device__ __forceinline__ Eq2 merge(const Eq2& A, const Eq2& B, int64_t row_t, G& bad,
                                      MergeSave& sv) {
     Eq2 P;
     // up-sweep: seed row 2 (= B.E1), then row 1 (= A.E2), then row 0 (= A.E1)
-    check_pivot(B.b1, row_t + 1, bad);
+    bad.see(B.b1, row_t + 1);
     const double w1 = A.g2 * rcp(B.b1);
     const double beta1 = A.b2 - w1 * B.a1;
     const double gamma1 = -w1 * B.g1;
     const double delta1 = A.d2 - w1 * B.d1;
-    check_pivot(beta1, row_t, bad);
+    bad.see(beta1, row_t);
     const double r1 = rcp(beta1);
     const double w0 = A.g1 * r1;
     P.a1 = A.a1;
@@ -203,12 +224,12 @@ __device__ __forceinline__ Eq2 merge(const Eq2& A, const Eq2& B, int64_t row_t, 
     P.g1 = -w0 * gamma1;
     P.d1 = A.d1 - w0 * delta1;
     // down-sweep: seed row 1 (= A.E2), then rows 2, 3
-    check_pivot(A.b2, row_t, bad);
+    bad.see(A.b2, row_t);
     const double w2 = B.a1 * rcp(A.b2);
     const double phi = -w2 * A.a2;
     const double bp = B.b1 - w2 * A.g2;
     const double dp = B.d1 - w2 * A.d2;
-    check_pivot(bp, row_t + 1, bad);
+    bad.see(bp, row_t + 1);
     const double w3 = B.a2 * rcp(bp);
     P.a2 = -w3 * phi;
     P.b2 = B.b2 - w3 * B.g1;
@@ -233,14 +254,15 @@ __device__ __forceinline__ double first_from_e1(const Eq2& B, double xt, double 
 // Solve the 2x2 root system of a whole (non-coupled) system by Thomas
 // (tridiagonal.hpp:52-72 on [E1; E2]); sub of row 0 / super of row 1 ignored,
 // exactly as thomas_solve never reads sub[0] and drops c'_{n-1}.
-__device__ __forceinline__ void root_solve(const Eq2& q, int64_t row_last, int64_t& bad,
+template <class G>
+__device__ __forceinline__ void root_solve(const Eq2& q, int64_t row_last, G& bad,
                                            double& x0, double& x1) {
-    check_pivot(q.b1, 0, bad);
+    bad.see(q.b1, 0);
     const double r0 = rcp(q.b1);
     const double cm = q.g1 * r0;
     const double xp = q.d1 * r0;
     const double piv = q.b2 - q.a2 * cm;
-    check_pivot(piv, row_last, bad);
+    bad.see(piv, row_last);
     x1 = (q.d2 - q.a2 * xp) * rcp(piv);
     x0 = xp - cm * x1;
 }

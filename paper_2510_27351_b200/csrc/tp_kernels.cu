@@ -14,107 +14,9 @@
 
 #include "tp_device.cuh"
 #include "tp_kernels.h"
+#include "tp_fast.cuh"
 
 namespace tpb {
-
-// ===========================================================================
-// Fast path: full blocks of m = L*G rows, one chunk of L rows per thread held
-// in registers, G lanes per block (G | 32), lane-tree merges via shuffles.
-// ===========================================================================
-template <int L, int G, int MODE, bool VEC>
-__global__ void __launch_bounds__(kFastThreads) k_fast(SysPtrs sys, int64_t nblocks, IfacePtrs out,
-                                                       const double* __restrict__ xi,
-                                                       double* __restrict__ x,
-                                                       unsigned long long* err, int level) {
-    static_assert(32 % G == 0, "G must divide the warp");
-    constexpr int LOGG = (G >= 32) ? 5 : (G >= 16) ? 4 : (G >= 8) ? 3 : (G >= 4) ? 2 : (G >= 2) ? 1 : 0;
-    const int64_t nchunks = nblocks * G;
-    const int lane = threadIdx.x & 31;
-    const int c = lane % G;  // chunk index inside the block
-    int64_t bad = INT64_MAX;
-
-    for (int64_t base = (int64_t)blockIdx.x * kFastThreads; base < nchunks;
-         base += (int64_t)gridDim.x * kFastThreads) {
-        const int64_t t = base + threadIdx.x;
-        // warp-uniform liveness: groups never straddle the nchunks boundary
-        const bool active = t < nchunks;
-        const int64_t row0 = t * L;
-        Chunk<L> r;
-        if (active) {
-            load_rows<L, VEC>(sys.sub, row0, r.a);
-            load_rows<L, VEC>(sys.diag, row0, r.b);
-            load_rows<L, VEC>(sys.sup, row0, r.c);
-            load_rows<L, VEC>(sys.rhs, row0, r.d);
-        } else {
-#pragma unroll
-            for (int i = 0; i < L; ++i) { r.a[i] = 0; r.b[i] = 1; r.c[i] = 0; r.d[i] = 0; }
-        }
-        const int64_t blk = t / G;
-
-        if constexpr (MODE == kStage1) {
-            int64_t lbad = INT64_MAX;
-            Eq2 cur = leaf_reduce<L>(r, L, row0, lbad);
-#pragma unroll
-            for (int lv = 0; lv < LOGG; ++lv) {
-                const int h = 1 << lv;
-                const Eq2 oth = shfl_down_eq(cur, h);
-                if ((c & (2 * h - 1)) == 0) {
-                    MergeSave sv;
-                    cur = merge(cur, oth, row0 + (int64_t)h * L - 1, lbad, sv);
-                }
-            }
-            if (active) {
-                bad = lbad < bad ? lbad : bad;
-                if (c == 0) {
-                    const int64_t o = 2 * blk;
-                    *reinterpret_cast<double2*>(out.sub + o) = make_double2(cur.a1, cur.a2);
-                    *reinterpret_cast<double2*>(out.diag + o) = make_double2(cur.b1, cur.b2);
-                    *reinterpret_cast<double2*>(out.sup + o) = make_double2(cur.g1, cur.g2);
-                    *reinterpret_cast<double2*>(out.rhs + o) = make_double2(cur.d1, cur.d2);
-                }
-            }
-        } else {
-            int64_t lbad = INT64_MAX;
-            double rbeta[L], gam[L], del[L];
-            Eq2 cur = leaf_reduce_keep<L>(r, L, row0, lbad, rbeta, gam, del);
-            MergeSave sv[LOGG > 0 ? LOGG : 1];
-#pragma unroll
-            for (int lv = 0; lv < LOGG; ++lv) {
-                const int h = 1 << lv;
-                const Eq2 oth = shfl_down_eq(cur, h);
-                if ((c & (2 * h - 1)) == 0) cur = merge(cur, oth, row0 + (int64_t)h * L - 1, lbad, sv[lv]);
-            }
-            // block ends from the next level's solution
-            double xs = 0, xe = 0;
-            if (c == 0 && active) {
-                const double2 v = *reinterpret_cast<const double2*>(xi + 2 * blk);
-                xs = v.x;
-                xe = v.y;
-            }
-#pragma unroll
-            for (int lv = LOGG - 1; lv >= 0; --lv) {
-                const int h = 1 << lv;
-                double xt = 0;
-                if ((c & (2 * h - 1)) == 0) xt = merge_xt(sv[lv], xs, xe);
-                const double rxt = __shfl_up_sync(0xffffffffu, xt, h);
-                const double rxe = __shfl_up_sync(0xffffffffu, xe, h);
-                if ((c & (2 * h - 1)) == h) {
-                    xs = first_from_e1(cur, rxt, rxe);
-                    xe = rxe;
-                } else if ((c & (2 * h - 1)) == 0) {
-                    xe = xt;
-                }
-            }
-            double xv[L];
-            leaf_expand<L>(r, L, rbeta, gam, del, xs, xe, xv);
-            if (active) {
-                bad = lbad < bad ? lbad : bad;
-                store_rows<L, VEC>(x, row0, xv);
-            }
-        }
-    }
-    report_pivot(err, level, bad);
-}
 
 // ===========================================================================
 // Generic path: any block length, rows staged through shared memory.
@@ -135,7 +37,7 @@ struct GenShared {
 // c <- gamma, d <- delta for the interior rows (consumed by leaf expansion).
 template <bool KEEP>
 __device__ Eq2 leaf_smem(double* a, double* b, double* c, double* d, int len, int64_t grow0,
-                         int64_t& bad) {
+                         RowGuard& bad) {
     Eq2 q;
     if (len == 1) {  // only in the n == 1 solve
         q.a1 = a[0]; q.b1 = b[0]; q.g1 = c[0]; q.d1 = d[0];
@@ -145,7 +47,7 @@ __device__ Eq2 leaf_smem(double* a, double* b, double* c, double* d, int len, in
     // down-sweep first (reads originals): partition.hpp:110-124
     double phi = a[1], bp = b[1], dp = d[1];
     for (int i = 2; i < len; ++i) {
-        check_pivot(bp, grow0 + i - 1, bad);
+        bad.see(bp, grow0 + i - 1);
         const double w = a[i] * rcp(bp);
         phi = -w * phi;
         bp = b[i] - w * c[i - 1];
@@ -159,7 +61,7 @@ __device__ Eq2 leaf_smem(double* a, double* b, double* c, double* d, int len, in
     double beta = b[len - 2], gamma = c[len - 2], delta = d[len - 2];
     if (KEEP) { c[len - 2] = gamma; d[len - 2] = delta; }
     for (int i = len - 3; i >= 0; --i) {
-        check_pivot(beta, grow0 + i + 1, bad);
+        bad.see(beta, grow0 + i + 1);
         const double rb = rcp(beta);
         const double w = c[i] * rb;
         const double nb = b[i] - w * a[i + 1];
@@ -201,7 +103,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
     const int64_t off = c * Llo + (c < ext ? c : ext);
     int logg = 0;
     while ((1 << logg) < G) ++logg;
-    int64_t bad = INT64_MAX;
+    RowGuard bad;
     constexpr bool KEEP = (MODE != kStage1);
 
     const int64_t ntiles = (nblocks + bpc - 1) / bpc;
@@ -261,7 +163,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
                 xe = xi[2 * jb + 1];
             } else {  // kSolve: the whole system is this one block
                 if (blen == 1) {
-                    check_pivot(cur.b1, 0, bad);
+                    bad.see(cur.b1, 0);
                     xs = xe = cur.d1 * rcp(cur.b1);
                 } else {
                     root_solve(cur, blen - 1, bad, xs, xe);
@@ -316,7 +218,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
         __syncthreads();
         (void)lane;
     }
-    report_pivot(err, level, bad);
+    report_pivot(err, level, bad.bad);
 }
 
 // ===========================================================================
@@ -332,18 +234,18 @@ __global__ void k_gather_solve(const double* __restrict__ eqs, int nranks, int r
     const int n = 2 * nranks;
     double* cm = scratch;
     double* xx = scratch + n;
-    int64_t bad = INT64_MAX;
+    RowGuard bad;
     for (int i = 0; i < n; ++i) {
         const double* e = eqs + 8 * (i >> 1);
         const int k = i & 1;
         const double sub = e[0 + k], dg = e[2 + k], sp = e[4 + k], rh = e[6 + k];
         if (i == 0) {
-            check_pivot(dg, 0, bad);
+            bad.see(dg, 0);
             cm[0] = sp / dg;
             xx[0] = rh / dg;
         } else {
             const double piv = dg - sub * cm[i - 1];
-            check_pivot(piv, i, bad);
+            bad.see(piv, i);
             cm[i] = sp / piv;
             xx[i] = (rh - sub * xx[i - 1]) / piv;
         }
@@ -351,7 +253,7 @@ __global__ void k_gather_solve(const double* __restrict__ eqs, int nranks, int r
     for (int i = n - 2; i >= 0; --i) xx[i] -= cm[i] * xx[i + 1];
     x2[0] = xx[2 * rank];
     x2[1] = xx[2 * rank + 1];
-    report_pivot(err, level, bad);
+    report_pivot(err, level, bad.bad);
 }
 
 // ===========================================================================
@@ -416,18 +318,36 @@ __global__ void k_residual(SysPtrs sys, int64_t n, const double* __restrict__ x,
 // ===========================================================================
 // Launchers
 // ===========================================================================
+// Launch shapes chosen by measurement (scratch/tune.cu on B200, N=1e8, m=64):
+// Stage 1  128 threads, <=80 regs (6 CTAs/SM), one chunk per thread (full grid)
+// Stage 3  128 threads, <=128 regs (4 CTAs/SM), persistent grid-stride
+template <int L, int G, int MODE, bool VEC>
+struct FastCfg {
+    static constexpr int kThreads = 128;
+    static constexpr int kMinBlocks = (MODE == kStage1) ? 6 : 4;
+    static constexpr bool kPersistent = (MODE != kStage1);
+    static void* fn() { return (void*)k_fast<L, G, MODE, VEC, kThreads, kMinBlocks>; }
+};
+
 template <int L, int G, bool VEC>
 static cudaError_t launch_fast_t(int mode, const SysPtrs& sys, int64_t nblocks, const IfacePtrs& out,
                                  const double* xi, double* x, unsigned long long* err, int level,
                                  int grid_cap, cudaStream_t st) {
     const int64_t nchunks = nblocks * G;
-    int64_t grid = (nchunks + kFastThreads - 1) / kFastThreads;
-    if (grid > grid_cap) grid = grid_cap;
-    if (grid < 1) grid = 1;
-    if (mode == kStage1)
-        k_fast<L, G, kStage1, VEC><<<(unsigned)grid, kFastThreads, 0, st>>>(sys, nblocks, out, xi, x, err, level);
-    else
-        k_fast<L, G, kStage3, VEC><<<(unsigned)grid, kFastThreads, 0, st>>>(sys, nblocks, out, xi, x, err, level);
+    if (mode == kStage1) {
+        using C = FastCfg<L, G, kStage1, VEC>;
+        int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
+        if (grid < 1) grid = 1;
+        k_fast<L, G, kStage1, VEC, C::kThreads, C::kMinBlocks><<<(unsigned)grid, C::kThreads, 0, st>>>(
+            sys, nblocks, out, xi, x, err, level);
+    } else {
+        using C = FastCfg<L, G, kStage3, VEC>;
+        int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
+        if (grid > grid_cap) grid = grid_cap;
+        if (grid < 1) grid = 1;
+        k_fast<L, G, kStage3, VEC, C::kThreads, C::kMinBlocks><<<(unsigned)grid, C::kThreads, 0, st>>>(
+            sys, nblocks, out, xi, x, err, level);
+    }
     return cudaGetLastError();
 }
 
@@ -542,11 +462,11 @@ int fast_max_active_blocks(int64_t m, bool vec, int mode) {
 #define TPB_OCC(MM, LL, GG)                                                                          \
     case MM:                                                                                         \
         if (mode == kStage1) {                                                                       \
-            if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast<LL, GG, kStage1, true>, kFastThreads, 0); \
-            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast<LL, GG, kStage1, false>, kFastThreads, 0); \
+            if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, FastCfg<LL, GG, kStage1, true>::fn(), 128, 0); \
+            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, FastCfg<LL, GG, kStage1, false>::fn(), 128, 0); \
         } else {                                                                                     \
-            if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast<LL, GG, kStage3, true>, kFastThreads, 0); \
-            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fast<LL, GG, kStage3, false>, kFastThreads, 0); \
+            if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, FastCfg<LL, GG, kStage3, true>::fn(), 128, 0); \
+            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, FastCfg<LL, GG, kStage3, false>::fn(), 128, 0); \
         }                                                                                            \
         break;
     switch (m) {

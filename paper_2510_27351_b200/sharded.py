@@ -22,7 +22,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 from ._lib import lib
-from .tridpart import RecursionPolicy, _call, _policy_array, _raise, context, predicted_policy
+from .tridpart import (RecursionPolicy, _call, _policy_array, _raise, context, predicted_policy,
+                       torch_stream)
 
 
 def shard_bounds(n_global: int, nranks: int, rank: int):
@@ -59,7 +60,7 @@ class DeviceBackend:
 
         sz = _policy_array(policy)
         eq8 = torch.empty(8, dtype=torch.float64, device=sys4[0].device)
-        stream = torch.cuda.current_stream().cuda_stream
+        stream = torch_stream()
         _call(lib.tp_shard_reduce_f64_dev, self.ctx.handle, *self._ptrs(sys4), int(sys4[0].numel()),
               sz.ctypes.data_as(C.POINTER(C.c_int64)), len(sz), C.c_void_p(eq8.data_ptr()),
               C.c_void_p(stream))
@@ -70,7 +71,7 @@ class DeviceBackend:
 
         sz = _policy_array(policy)
         x = out if out is not None else torch.empty_like(sys4[1])
-        stream = torch.cuda.current_stream().cuda_stream
+        stream = torch_stream()
         _call(lib.tp_shard_finish_f64_dev, self.ctx.handle, *self._ptrs(sys4), int(sys4[0].numel()),
               sz.ctypes.data_as(C.POINTER(C.c_int64)), len(sz), C.c_void_p(gathered.data_ptr()),
               int(nranks), int(rank), C.c_void_p(x.data_ptr()), C.c_void_p(stream))

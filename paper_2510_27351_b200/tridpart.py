@@ -171,6 +171,15 @@ def context(device: Optional[int] = None) -> Context:
     return cache[device]
 
 
+def torch_stream() -> int:
+    """cudaStream_t of torch's current stream. torch's default stream is the
+    legacy NULL stream: pass cudaStreamLegacy (0x1) for it, because a NULL
+    stream argument means "the context's own stream" in the C-ABI."""
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream or 0x1
+
+
 # ----------------------------------------------------------- tridiagonal.hpp
 def _is_torch(a) -> bool:
     return type(a).__module__.startswith("torch")
@@ -234,7 +243,7 @@ def generate_system(n: int, seed: int, delta: float = 1.5, device: bool = False,
     n_global = n if n_global is None else n_global
     ctx = context()
     arrs = [torch.empty(n, dtype=torch.float64, device=f"cuda:{ctx.device}") for _ in range(4)]
-    stream = torch.cuda.current_stream().cuda_stream
+    stream = torch_stream()
     _call(lib.tp_generate_system_f64_dev, ctx.handle, n, row0, n_global, C.c_uint64(seed), delta,
           *[C.c_void_p(a.data_ptr()) for a in arrs], C.c_void_p(stream))
     if device:
@@ -365,7 +374,7 @@ def solve_partition_async(sys: TridiagonalSystem, policy, out=None):
     ctx = context()
     n = sys.size()
     x = out if out is not None else torch.empty(n, dtype=torch.float64, device=sys.diag.device)
-    stream = torch.cuda.current_stream().cuda_stream
+    stream = torch_stream()
     _call(lib.tp_solve_partition_f64_dev, ctx.handle, *sys._dev_ptrs(), n, sz.ctypes.data_as(_I64),
           len(sz), C.c_void_p(x.data_ptr()), C.c_void_p(stream))
     return x
