@@ -256,10 +256,8 @@ struct Runner {
     }
 
     void final_solve(const Plan& p) {
-        const int G = generic_G(p.n_final, tpb::kFinalThreads);
-        const int T = std::max(32, G);
-        check(tpb::launch_generic(tpb::kSolve, T, G, 1, p.final_in, 0, 0, 1, p.n_final, IfacePtrs{},
-                                  nullptr, p.final_x, ctx->d_err, (int)p.levels.size(), st));
+        check(tpb::launch_final(tpb::kSolve, p.final_in, p.n_final, IfacePtrs{}, nullptr, p.final_x,
+                                ctx->d_err, (int)p.levels.size(), st));
         after("final", (int)p.levels.size());
     }
 
@@ -275,11 +273,9 @@ struct Runner {
     void shard_reduce(const Plan& p, double* eq8) {
         check(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
         for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
-        const int G = generic_G(p.n_final, tpb::kFinalThreads);
-        const int T = std::max(32, G);
         IfacePtrs o{eq8, eq8 + 2, eq8 + 4, eq8 + 6};
-        check(tpb::launch_generic(tpb::kStage1, T, G, 1, p.final_in, 0, 0, 1, p.n_final, o, nullptr,
-                                  nullptr, ctx->d_err, (int)p.levels.size(), st));
+        check(tpb::launch_final(tpb::kStage1, p.final_in, p.n_final, o, nullptr, nullptr, ctx->d_err,
+                                (int)p.levels.size(), st));
         after("shard_reduce", (int)p.levels.size());
     }
     void shard_finish(const Plan& p, const double* eq_all, int nranks, int rank) {
@@ -288,10 +284,8 @@ struct Runner {
         check(tpb::launch_gather_solve(eq_all, nranks, rank, x2, scratch, ctx->d_err,
                                        (int)p.levels.size() + 1, st));
         after("gather_solve", (int)p.levels.size() + 1);
-        const int G = generic_G(p.n_final, tpb::kFinalThreads);
-        const int T = std::max(32, G);
-        check(tpb::launch_generic(tpb::kStage3, T, G, 1, p.final_in, 0, 0, 1, p.n_final, IfacePtrs{},
-                                  x2, p.final_x, ctx->d_err, (int)p.levels.size(), st));
+        check(tpb::launch_final(tpb::kStage3, p.final_in, p.n_final, IfacePtrs{}, x2, p.final_x,
+                                ctx->d_err, (int)p.levels.size(), st));
         after("shard_expand", (int)p.levels.size());
         for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
     }

@@ -222,6 +222,189 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
 }
 
 // ===========================================================================
+// Finishing solve: ONE CTA solves (or reduces / expands) a whole system of
+// n <= kFinalCap rows held in shared memory. This replaces the reference's
+// sequential thomas_solve(iface) at the deepest level (partition.hpp:211) and
+// its n < 4 fallback (:197) with an exact parallel elimination:
+//   G chunks (one per thread, G a power of two) -> leaf sweeps from smem
+//   -> 5 warp-level merge levels via shuffles -> warp roots to smem
+//   -> warp 0 merges the warp roots (<= 4 more levels) and handles the root
+//   -> top-down the same tree -> leaf back-substitution -> coalesced store.
+// Modes: kSolve (2x2 root system solved, as Thomas on [E1;E2]),
+//        kStage1 (write the root E1/E2: the sharded reduce),
+//        kStage3 (root ends read from xi: the sharded expand).
+// ===========================================================================
+template <int MODE>
+__global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n, int G, IfacePtrs out,
+                                                         const double* __restrict__ xi,
+                                                         double* __restrict__ x,
+                                                         unsigned long long* err, int level) {
+    extern __shared__ __align__(16) double fsm[];
+    double* sa = fsm;
+    double* sb = sa + n;
+    double* sc = sb + n;
+    double* sd = sc + n;
+    __shared__ Eq2 wroot[kFinalThreads2 / 32];
+    __shared__ double wx[2 * (kFinalThreads2 / 32)];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    RowGuard bad;
+
+    if (n == 1) {  // thomas_solve on one row (tridiagonal.hpp:57-59)
+        if (tid == 0 && MODE == kSolve) {
+            bad.see(sys.diag[0], 0);
+            x[0] = sys.rhs[0] / sys.diag[0];
+        }
+        report_pivot(err, level, bad.bad);
+        return;
+    }
+    for (int64_t i = tid; i < n; i += kFinalThreads2) {
+        sa[i] = __ldg(sys.sub + i);
+        sb[i] = __ldg(sys.diag + i);
+        sc[i] = __ldg(sys.sup + i);
+        sd[i] = __ldg(sys.rhs + i);
+    }
+    __syncthreads();
+
+    const int Llo = (int)(n / G), ext = (int)(n % G);
+    const bool active = tid < G;
+    const int len = Llo + (tid < ext ? 1 : 0);
+    const int off = tid * Llo + (tid < ext ? tid : ext);
+    auto chunk_start = [&](int c) { return c * Llo + (c < ext ? c : ext); };
+    constexpr bool KEEP = (MODE != kStage1);
+
+    Eq2 cur = Eq2{0, 1, 0, 0, 0, 1, 0, 0};
+    if (active) cur = leaf_smem<KEEP>(sa + off, sb + off, sc + off, sd + off, len, off, bad);
+
+    // ---- warp-level tree (chunk index == tid) ----
+    MergeSave sw[5];
+#pragma unroll
+    for (int lv = 0; lv < 5; ++lv) {
+        const int h = 1 << lv;
+        const Eq2 oth = shfl_down_eq(cur, h);
+        if (h < G && (lane & (2 * h - 1)) == 0 && tid + h < G)
+            cur = merge(cur, oth, (int64_t)chunk_start(tid + h) - 1, bad, sw[lv]);
+    }
+    const int nwr = G >= 32 ? G / 32 : 1;  // warp roots
+    if (lane == 0 && warp < nwr) wroot[warp] = cur;
+    __syncthreads();
+
+    // ---- warp 0: merge the warp roots, handle the root, push ends back down ----
+    if (warp == 0) {
+        Eq2 wc = lane < nwr ? wroot[lane] : Eq2{0, 1, 0, 0, 0, 1, 0, 0};
+        MergeSave sx[5];
+#pragma unroll
+        for (int lv = 0; lv < 5; ++lv) {
+            const int h = 1 << lv;
+            const Eq2 oth = shfl_down_eq(wc, h);
+            if (h < nwr && (lane & (2 * h - 1)) == 0 && lane + h < nwr)
+                wc = merge(wc, oth, (int64_t)chunk_start(32 * (lane + h)) - 1, bad, sx[lv]);
+        }
+        double xs = 0, xe = 0;
+        if (lane == 0) {
+            if (MODE == kStage1) {
+                out.sub[0] = wc.a1;  out.sub[1] = wc.a2;
+                out.diag[0] = wc.b1; out.diag[1] = wc.b2;
+                out.sup[0] = wc.g1;  out.sup[1] = wc.g2;
+                out.rhs[0] = wc.d1;  out.rhs[1] = wc.d2;
+            } else if (MODE == kStage3) {
+                xs = xi[0];
+                xe = xi[1];
+            } else {
+                root_solve(wc, n - 1, bad, xs, xe);
+            }
+        }
+        if (MODE != kStage1) {
+#pragma unroll
+            for (int lv = 4; lv >= 0; --lv) {
+                const int h = 1 << lv;
+                if (h >= nwr) continue;
+                double xt = 0;
+                if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sx[lv], xs, xe);
+                const double rxt = __shfl_up_sync(0xffffffffu, xt, h);
+                const double rxe = __shfl_up_sync(0xffffffffu, xe, h);
+                if ((lane & (2 * h - 1)) == h) {
+                    xs = first_from_e1(wc, rxt, rxe);
+                    xe = rxe;
+                } else if ((lane & (2 * h - 1)) == 0) {
+                    xe = xt;
+                }
+            }
+            if (lane < nwr) {
+                wx[2 * lane] = xs;
+                wx[2 * lane + 1] = xe;
+            }
+        }
+    }
+    if (MODE == kStage1) {
+        report_pivot(err, level, bad.bad);
+        return;
+    }
+    __syncthreads();
+
+    // ---- every warp: its segment ends, then the warp-level tree top-down ----
+    double xs = 0, xe = 0;
+    if (lane == 0 && warp < nwr) {
+        xs = wx[2 * warp];
+        xe = wx[2 * warp + 1];
+    }
+#pragma unroll
+    for (int lv = 4; lv >= 0; --lv) {
+        const int h = 1 << lv;
+        if (h >= G) continue;
+        double xt = 0;
+        if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sw[lv], xs, xe);
+        const double rxt = __shfl_up_sync(0xffffffffu, xt, h);
+        const double rxe = __shfl_up_sync(0xffffffffu, xe, h);
+        if ((lane & (2 * h - 1)) == h) {
+            xs = first_from_e1(cur, rxt, rxe);
+            xe = rxe;
+        } else if ((lane & (2 * h - 1)) == 0) {
+            xe = xt;
+        }
+    }
+    // ---- leaf back-substitution into the a-slots, then a coalesced store ----
+    if (active) {
+        double* a = sa + off;
+        const double* rb = sb + off;
+        const double* g = sc + off;
+        const double* dd = sd + off;
+        double prev = xs;
+        for (int i = 1; i < len - 1; ++i) {
+            const double xv = (dd[i] - a[i] * prev - g[i] * xe) * rb[i];
+            a[i] = xv;
+            prev = xv;
+        }
+        a[0] = xs;
+        a[len - 1] = xe;
+    }
+    __syncthreads();
+    for (int64_t i = tid; i < n; i += kFinalThreads2) x[i] = sa[i];
+    report_pivot(err, level, bad.bad);
+}
+
+size_t final_smem_bytes(int64_t n) { return (size_t)(4 * n) * sizeof(double); }
+
+int final_G(int64_t n) {
+    int G = 1;
+    while (G * 2 <= kFinalThreads2 && n / (G * 2) >= 2) G *= 2;
+    return G;
+}
+
+cudaError_t launch_final(int mode, const SysPtrs& sys, int64_t n, const IfacePtrs& out, const double* xi,
+                         double* x, unsigned long long* err, int level, cudaStream_t st) {
+    if (n > kFinalCap || n < 1) return cudaErrorInvalidValue;
+    const int G = final_G(n);
+    const size_t smem = final_smem_bytes(n);
+    if (mode == kStage1)
+        k_final<kStage1><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
+    else if (mode == kStage3)
+        k_final<kStage3><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
+    else
+        k_final<kSolve><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
+    return cudaGetLastError();
+}
+
+// ===========================================================================
 // Sharded top level: every rank holds the gathered [eq8 x P] (layout per rank:
 // sub[2], diag[2], sup[2], rhs[2]); assemble the 2P-row interface
 // (assemble_interface, partition.hpp:139-149) and solve it with Thomas
@@ -428,6 +611,10 @@ cudaError_t init_kernel_attributes() {
     cudaError_t e = cudaFuncSetAttribute(k_generic<kStage1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_generic<kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_generic<kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+    const int fs = (int)(kMaxDynSmem - 4096);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<kStage1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
     return e;
 }
 

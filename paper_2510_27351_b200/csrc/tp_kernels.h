@@ -12,7 +12,8 @@ constexpr int kSolve = 2;   // whole system as one block: reduce, 2x2 root, expa
 
 constexpr int kFastThreads = 256;
 constexpr int kGenericThreads = 256;
-constexpr int kFinalThreads = 1024;
+constexpr int kFinalThreads = 1024;   // k_generic CTA cap
+constexpr int kFinalThreads2 = 512;   // k_final CTA
 // Largest system the single-CTA finishing solve keeps in shared memory
 // (32 B per row; 6144 rows = 192 KiB of the 227 KiB opt-in limit).
 constexpr int64_t kFinalCap = 6144;
@@ -43,6 +44,8 @@ cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs
                            int64_t blk_base, int64_t nblocks, int64_t blen, const IfacePtrs& out,
                            const double* xi, double* x, unsigned long long* err, int level,
                            cudaStream_t st);
+cudaError_t launch_final(int mode, const SysPtrs& sys, int64_t n, const IfacePtrs& out, const double* xi,
+                         double* x, unsigned long long* err, int level, cudaStream_t st);
 cudaError_t launch_gather_solve(const double* eqs, int nranks, int rank, double* x2, double* scratch,
                                 unsigned long long* err, int level, cudaStream_t st);
 cudaError_t launch_generate(int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
