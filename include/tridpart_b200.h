@@ -150,6 +150,10 @@ tp_status tp_solve_profile_f64_dev(tp_ctx* ctx, const double* sub, const double*
                                    float* kernel_ms, char* names /* [max_kernels][32] */,
                                    int32_t max_kernels, int32_t* nkernels, tp_error* err);
 
+/* Diagnostic: max ulp distance between the solver's reciprocal (MUFU.RCP64H +
+ * one cubic Newton step) and the correctly rounded 1/x over n random x. */
+int tp_diag_rcp_ulp(int64_t n, uint64_t seed, uint64_t* max_ulp);
+
 /* ------------------------------------------------------ kNN predictors */
 /* predict(model, n) — knn.hpp:57-77 (feature_of :38): k-NN on log10(N);
  * distance ties -> smaller N, vote ties -> smaller label. Host code. */

@@ -37,7 +37,7 @@ EXPORTS = [
     "tp_residual_inf_f64_dev", "tp_shard_reduce_f64_dev", "tp_shard_finish_f64_dev",
     "tp_generate_system_f64_dev", "tp_make_plan", "tp_plan_levels", "tp_solve_profile_f64_dev",
     "tp_predict", "tp_fit_knn", "tp_recursion_sizes", "tp_default_model", "tp_obs_read",
-    "tp_obs_get", "tp_obs_free",
+    "tp_obs_get", "tp_obs_free", "tp_diag_rcp_ulp",
 ]
 
 
@@ -81,6 +81,7 @@ def _load():
         "tp_obs_read": (C.c_int, [C.c_char_p, C.POINTER(vp), _I64, E]),
         "tp_obs_get": (C.c_int, [vp, C.c_int64, C.POINTER(TpObservation), _I32, _D, E]),
         "tp_obs_free": (None, [vp]),
+        "tp_diag_rcp_ulp": (C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

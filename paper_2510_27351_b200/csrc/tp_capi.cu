@@ -168,6 +168,8 @@ struct tp_ctx {
     int device = 0;
     int sms = 148;
     cudaStream_t own = nullptr;
+    cudaStream_t side = nullptr;  // tail-block branch
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t stream = nullptr;
     bool graphs = true;
     double* ws = nullptr;
@@ -225,34 +227,51 @@ struct Runner {
         if (e != cudaSuccess && status == cudaSuccess) status = e;
     }
 
-    void stage(const Level& L, int level, int mode) {
+    void main_part(const Level& L, int level, int mode) {
         const bool s1 = (mode == tpb::kStage1);
-        if (L.kfull > 0) {
-            int fl, fg;
-            if (tpb::fast_shape(L.m, &fl, &fg)) {
-                const bool vec = aligned32(L.in.sub) && aligned32(L.in.diag) && aligned32(L.in.sup) &&
-                                 aligned32(L.in.rhs) && (s1 || aligned32(L.x_out));
-                check(tpb::launch_fast(L.m, vec, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
-                                       ctx->d_err, level, fast_grid_cap(ctx, L.m, vec, mode), st));
-                after(s1 ? "stage1" : "stage3", level);
-            } else {
-                const int T = tpb::kGenericThreads;
-                const int G = generic_G(L.m, T);
-                const int64_t bpc = T / G;
-                int64_t grid = (L.kfull + bpc - 1) / bpc;
-                grid = std::min<int64_t>(grid, (int64_t)ctx->sms * 8);
-                check(tpb::launch_generic(mode, T, G, (int)grid, L.in, 0, 0, L.kfull, L.m, L.iface,
-                                          L.x_iface, L.x_out, ctx->d_err, level, st));
-                after(s1 ? "stage1g" : "stage3g", level);
-            }
-        }
-        if (L.tail > 0) {
-            const int G = generic_G(L.tail, tpb::kGenericThreads);
-            const int T = std::max(32, G);
-            check(tpb::launch_generic(mode, T, G, 1, L.in, L.kfull * L.m, L.kfull, 1, L.tail, L.iface,
+        int fl, fg;
+        if (tpb::fast_shape(L.m, &fl, &fg)) {
+            const bool vec = aligned32(L.in.sub) && aligned32(L.in.diag) && aligned32(L.in.sup) &&
+                             aligned32(L.in.rhs) && (s1 || aligned32(L.x_out));
+            check(tpb::launch_fast(L.m, vec, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
+                                   ctx->d_err, level, fast_grid_cap(ctx, L.m, vec, mode), st));
+            after(s1 ? "stage1" : "stage3", level);
+        } else {
+            const int T = tpb::kGenericThreads;
+            const int G = generic_G(L.m, T);
+            const int64_t bpc = T / G;
+            int64_t grid = (L.kfull + bpc - 1) / bpc;
+            grid = std::min<int64_t>(grid, (int64_t)ctx->sms * 8);
+            check(tpb::launch_generic(mode, T, G, (int)grid, L.in, 0, 0, L.kfull, L.m, L.iface,
                                       L.x_iface, L.x_out, ctx->d_err, level, st));
-            after(s1 ? "stage1t" : "stage3t", level);
+            after(s1 ? "stage1g" : "stage3g", level);
         }
+    }
+    void tail_part(const Level& L, int level, int mode, cudaStream_t s) {
+        const int G = generic_G(L.tail, tpb::kGenericThreads);
+        const int T = std::max(32, G);
+        check(tpb::launch_generic(mode, T, G, 1, L.in, L.kfull * L.m, L.kfull, 1, L.tail, L.iface,
+                                  L.x_iface, L.x_out, ctx->d_err, level, s));
+        after(mode == tpb::kStage1 ? "stage1t" : "stage3t", level);
+    }
+
+    // One level of Stage 1 or Stage 3. The tail block (make_plan's last block
+    // when its length != m) is independent of the full blocks, so it runs on a
+    // forked stream (a parallel branch of the captured graph) and joins before
+    // the next dependent kernel. The instrumented path keeps them serial.
+    void stage(const Level& L, int level, int mode) {
+        const bool fork = L.kfull > 0 && L.tail > 0 && hook == nullptr;
+        if (fork) {
+            check(cudaEventRecord(ctx->ev_fork, st));
+            check(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            tail_part(L, level, mode, ctx->side);
+            check(cudaEventRecord(ctx->ev_join, ctx->side));
+            main_part(L, level, mode);
+            check(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+            return;
+        }
+        if (L.kfull > 0) main_part(L, level, mode);
+        if (L.tail > 0) tail_part(L, level, mode, st);
     }
 
     void final_solve(const Plan& p) {
@@ -475,6 +494,9 @@ tp_status tp_ctx_create(int32_t device, tp_ctx** out, tp_error* err) {
     c->device = device;
     c->sms = prop.multiProcessorCount;
     cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 64);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_red, 64);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_small, 4096);
@@ -500,6 +522,9 @@ void tp_ctx_destroy(tp_ctx* ctx) {
     if (ctx->d_small) cudaFree(ctx->d_small);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->own) cudaStreamDestroy(ctx->own);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     delete ctx;
 }
 

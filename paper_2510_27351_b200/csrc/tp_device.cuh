@@ -39,17 +39,17 @@ struct MergeSave {
     double d1, g1, r1, a2;
 };
 
-// FP64 reciprocal: MUFU.RCP64H seed + two Newton steps (error ~1 ulp); no
-// slow path, because every pivot it sees passed the |p| >= 1e-30 floor check
-// (or is already reported as a zero pivot). w = c * rcp(p) replaces the
-// reference's c / p (<= ~2 ulp apart; parity is by tolerance).
+// FP64 reciprocal: MUFU.RCP64H seed + one cubic Newton step, <= 1 ulp from the
+// correctly rounded 1/x (checked on the GPU by tp_diag_rcp_ulp); no slow path,
+// because every pivot it sees passed the |p| >= 1e-30 floor check (or is
+// already reported as a zero pivot). w = c * rcp(p) replaces the reference's
+// c / p (<= ~2 ulp apart; parity is by tolerance).
 __device__ __forceinline__ double rcp(double x) {
+    // seed error e0 ~ 2^-22; r*(1 + e + e^2) leaves ~e0^3 before rounding
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
+    const double e = fma(-x, r, 1.0);
+    return fma(r, fma(e, e, e), r);
 }
 
 // Zero-pivot bookkeeping (|pivot| < kPivotFloor -> ZeroPivotError).

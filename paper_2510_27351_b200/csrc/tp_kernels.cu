@@ -257,11 +257,32 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
         report_pivot(err, level, bad.bad);
         return;
     }
-    for (int64_t i = tid; i < n; i += kFinalThreads2) {
-        sa[i] = __ldg(sys.sub + i);
-        sb[i] = __ldg(sys.diag + i);
-        sc[i] = __ldg(sys.sup + i);
-        sd[i] = __ldg(sys.rhs + i);
+    // all of a thread's loads are issued before its first shared-memory store
+    // (kFinalCap / kFinalThreads2 = 12 rows per thread), so the L2 latency is
+    // paid once, not once per row
+    {
+        constexpr int kPer = (int)((kFinalCap + kFinalThreads2 - 1) / kFinalThreads2);
+        double va[kPer], vb[kPer], vc[kPer], vd[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int64_t i = tid + (int64_t)k * kFinalThreads2;
+            if (i < n) {
+                va[k] = __ldg(sys.sub + i);
+                vb[k] = __ldg(sys.diag + i);
+                vc[k] = __ldg(sys.sup + i);
+                vd[k] = __ldg(sys.rhs + i);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int64_t i = tid + (int64_t)k * kFinalThreads2;
+            if (i < n) {
+                sa[i] = va[k];
+                sb[i] = vb[k];
+                sc[i] = vc[k];
+                sd[i] = vd[k];
+            }
+        }
     }
     __syncthreads();
 
@@ -677,3 +698,36 @@ int fast_max_active_blocks(int64_t m, bool vec, int mode) {
 }
 
 }  // namespace tpb
+
+namespace tpb {
+// Diagnostic: max distance in ulps between rcp(x) and the correctly rounded
+// 1/x over `n` pseudo-random x spanning [1e-30, 1e30) with random sign.
+__global__ void k_diag_rcp(int64_t n, uint64_t seed, unsigned long long* max_ulp) {
+    unsigned long long worst = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = mix64(seed ^ (uint64_t)i * 0x9E3779B97F4A7C15ULL);
+        const double u = canon(h);
+        double x = exp10(60.0 * u - 30.0);
+        if (h & 1) x = -x;
+        const double a = rcp(x), b = __drcp_rn(x);
+        const long long ia = __double_as_longlong(a), ib = __double_as_longlong(b);
+        const unsigned long long d = (unsigned long long)(ia > ib ? ia - ib : ib - ia);
+        worst = d > worst ? d : worst;
+    }
+    atomicMax(max_ulp, worst);
+}
+}  // namespace tpb
+
+extern "C" int tp_diag_rcp_ulp(int64_t n, uint64_t seed, uint64_t* max_ulp) {
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return 9;
+    cudaMemset(d, 0, sizeof(unsigned long long));
+    tpb::k_diag_rcp<<<148 * 4, 256>>>(n, seed, d);
+    unsigned long long h = 0;
+    const cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return 9;
+    *max_ulp = h;
+    return 0;
+}

@@ -266,3 +266,14 @@ def test_sharded_solve_on_one_gpu(tp, oracle_mod):
     for P in (1, 2, 3, 8):
         x = sharded.simulate_ranks(s.sub, s.diag, s.sup, s.rhs, P)
         _check(oracle_mod, s, x, ref)
+
+
+def test_reciprocal_is_within_one_ulp(tp):
+    import ctypes as C
+
+    from paper_2510_27351_b200._lib import lib
+
+    tp.context()
+    worst = C.c_uint64()
+    assert lib.tp_diag_rcp_ulp(10_000_000, 7, C.byref(worst)) == 0
+    assert worst.value <= 1, worst.value
