@@ -354,7 +354,7 @@ def run_ours(args):
         peak, peak_src = hbm_peak()
         roof = None
         if prof:
-            k = "stage3:L0"
+            k = "stage3:L0"  # the dominant kernel
             t_k = prof.get(k)
             achieved = ALG_BYTES_PER_UNKNOWN * n_loc / (t_k * 1e-3) / 1e9
             traffic = None
@@ -362,7 +362,7 @@ def run_ours(args):
             if os.path.exists(summ):
                 try:
                     with open(summ) as f:
-                        traffic = json.load(f).get("stage3_L0", {}).get("dram_bytes")
+                        traffic = json.load(f).get(k, {}).get("dram_bytes")
                 except Exception:
                     traffic = None
             roof = {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -281,8 +281,25 @@ struct Runner {
     }
 
     // Whole solve (reset error word, Stage 1 down, finish, Stage 3 up).
+    // k_generic over blocks [blk0, blk0 + nblocks) of length blen of one level.
+    void generic_range(int mode, const Level& L, int64_t blk0, int64_t nblocks, int64_t blen,
+                       int level, cudaStream_t s, const char* name) {
+        if (nblocks <= 0) return;
+        const int G = generic_G(blen, tpb::kGenericThreads);
+        const int T = nblocks == 1 ? std::max(32, G) : tpb::kGenericThreads;
+        const int64_t bpc = T / G;
+        int64_t grid = (nblocks + bpc - 1) / bpc;
+        grid = std::min<int64_t>(grid, (int64_t)ctx->sms * 8);
+        check(tpb::launch_generic(mode, T, G, (int)grid, L.in, blk0 * L.m, blk0, nblocks, blen,
+                                  L.iface, L.x_iface, L.x_out, ctx->d_err, level, s));
+        after(name, level);
+    }
+
     void solve(const Plan& p) {
         check(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
+        solve_body(p);
+    }
+    void solve_body(const Plan& p) {
         for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
         final_solve(p);
         for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
@@ -549,6 +566,7 @@ tp_status tp_ctx_set_graphs(tp_ctx* ctx, int32_t enabled, tp_error* err) {
 }
 
 int64_t tp_ctx_last_launch_count(const tp_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
 
 tp_status tp_solve_partition_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
                                      const double* super, const double* rhs, int64_t n,
@@ -880,9 +898,7 @@ tp_status tp_solve_profile_f64_dev(tp_ctx* ctx, const double* sub, const double*
     Runner r{ctx, st};
     r.hook = profile_hook;
     r.hook_user = &ps;
-    for (size_t l = 0; l < p.levels.size(); ++l) r.stage(p.levels[l], (int)l, tpb::kStage1);
-    r.final_solve(p);
-    for (size_t l = p.levels.size(); l-- > 0;) r.stage(p.levels[l], (int)l, tpb::kStage3);
+    r.solve_body(p);
     ctx->last_launches = r.launches;
     TP_CUDA(cudaStreamSynchronize(st));
     const int32_t cnt = (int32_t)std::min<size_t>(ps.evs.size(), (size_t)max_kernels);

@@ -277,3 +277,4 @@ def test_reciprocal_is_within_one_ulp(tp):
     worst = C.c_uint64()
     assert lib.tp_diag_rcp_ulp(10_000_000, 7, C.byref(worst)) == 0
     assert worst.value <= 1, worst.value
+
