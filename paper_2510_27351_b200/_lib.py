@@ -7,7 +7,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtridpart_b200.so")
+# TPB_LIB overrides the library path (A/B experiments between two builds)
+LIB_PATH = os.environ.get("TPB_LIB") or os.path.join(HERE, "lib", "libtridpart_b200.so")
 
 _D = C.POINTER(C.c_double)
 _I64 = C.POINTER(C.c_int64)
