@@ -236,6 +236,10 @@ struct Runner {
             check(tpb::launch_fast(L.m, vec, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
                                    ctx->d_err, level, fast_grid_cap(ctx, L.m, vec, mode), st));
             after(s1 ? "stage1" : "stage3", level);
+        } else if (tpb::fast_rt_G(L.m) > 0) {
+            check(tpb::launch_fast_rt(L.m, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out, ctx->d_err,
+                                      level, ctx->sms, st));
+            after(s1 ? "stage1r" : "stage3r", level);
         } else {
             const int T = tpb::kGenericThreads;
             const int G = generic_G(L.m, T);

@@ -80,7 +80,8 @@ __device__ __forceinline__ void report_pivot(unsigned long long* err, int level,
 }
 
 // ---------------------------------------------------------------------------
-// Leaf: one chunk of L rows held in registers (L compile-time, len <= L valid).
+// Leaf: one chunk held in registers sized L; its first K rows are valid
+// (K == L on the fixed-shape path; k_fast_rt dispatches on a runtime length).
 // up-sweep  = partition.hpp:90-108, down-sweep = partition.hpp:110-124.
 // ---------------------------------------------------------------------------
 template <int L>
@@ -89,8 +90,8 @@ struct Chunk {
 };
 
 // Stage-1 leaf: E1/E2 only (no per-row storage).
-template <int L, class G>
-__device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int len, int64_t row0, G& bad) {
+template <int L, int len, class G>
+__device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int64_t row0, G& bad) {
     Eq2 q;
     // up-sweep: seed row len-2, run i = len-3 .. 0
     double beta = 0, gamma = 0, delta = 0;
@@ -135,8 +136,8 @@ __device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int len, int64_t r
 
 // Stage-3 leaf: same sweeps, but keeps rcp(beta_i), gamma_i, delta_i of the
 // interior rows for back_substitute (partition.hpp:156-172).
-template <int L, class G>
-__device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int len, int64_t row0,
+template <int L, int len, class G>
+__device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int64_t row0,
                                                 G& bad, double (&rbeta)[L],
                                                 double (&gam)[L], double (&del)[L]) {
     Eq2 q;
@@ -184,8 +185,8 @@ __device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int len, int6
 }
 
 // Interior of a chunk from its end values: back_substitute, partition.hpp:163-170.
-template <int L>
-__device__ __forceinline__ void leaf_expand(const Chunk<L>& r, int len, const double (&rbeta)[L],
+template <int L, int len>
+__device__ __forceinline__ void leaf_expand(const Chunk<L>& r, const double (&rbeta)[L],
                                             const double (&gam)[L], const double (&del)[L],
                                             double xs, double xe, double (&x)[L]) {
     x[0] = xs;

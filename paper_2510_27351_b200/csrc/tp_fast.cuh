@@ -34,14 +34,18 @@ __device__ __forceinline__ void load_chunk(const SysPtrs& sys, int64_t row0, boo
 }
 
 // Leaf sweeps + the G-lane merge tree; the block's pair ends up in lane c == 0.
-template <int L, int G, bool KEEP>
-__device__ __forceinline__ void lanes_up(LaneState<L, G, KEEP>& s, int c, int64_t row0) {
-    constexpr int LOGG = LaneState<L, G, KEEP>::LOGG;
+template <int L, int G, bool KEEP, int K = L>
+__device__ __forceinline__ void lane_leaf(LaneState<L, G, KEEP>& s, int64_t row0) {
     if constexpr (KEEP) {
-        s.cur = leaf_reduce_keep<L>(s.r, L, row0, s.guard, s.rbeta, s.gam, s.del);
+        s.cur = leaf_reduce_keep<L, K>(s.r, row0, s.guard, s.rbeta, s.gam, s.del);
     } else {
-        s.cur = leaf_reduce<L>(s.r, L, row0, s.guard);
+        s.cur = leaf_reduce<L, K>(s.r, row0, s.guard);
     }
+}
+
+template <int L, int G, bool KEEP>
+__device__ __forceinline__ void lanes_tree(LaneState<L, G, KEEP>& s, int c, int64_t row0) {
+    constexpr int LOGG = LaneState<L, G, KEEP>::LOGG;
 #pragma unroll
     for (int lv = 0; lv < LOGG; ++lv) {
         const int h = 1 << lv;
@@ -50,11 +54,16 @@ __device__ __forceinline__ void lanes_up(LaneState<L, G, KEEP>& s, int c, int64_
     }
 }
 
+template <int L, int G, bool KEEP>
+__device__ __forceinline__ void lanes_up(LaneState<L, G, KEEP>& s, int c, int64_t row0) {
+    lane_leaf<L, G, KEEP>(s, row0);
+    lanes_tree<L, G, KEEP>(s, c, row0);
+}
+
 // Top-down from the block ends (held by lane c == 0) and the chunk's
 // back-substitution; returns the chunk's L solution values.
 template <int L, int G>
-__device__ __forceinline__ void lanes_down(LaneState<L, G, true>& s, int c, double xs, double xe,
-                                           double (&xv)[L]) {
+__device__ __forceinline__ void lanes_tree_down(LaneState<L, G, true>& s, int c, double& xs, double& xe) {
     constexpr int LOGG = LaneState<L, G, true>::LOGG;
 #pragma unroll
     for (int lv = LOGG - 1; lv >= 0; --lv) {
@@ -70,7 +79,13 @@ __device__ __forceinline__ void lanes_down(LaneState<L, G, true>& s, int c, doub
             xe = xt;
         }
     }
-    leaf_expand<L>(s.r, L, s.rbeta, s.gam, s.del, xs, xe, xv);
+}
+
+template <int L, int G>
+__device__ __forceinline__ void lanes_down(LaneState<L, G, true>& s, int c, double xs, double xe,
+                                           double (&xv)[L]) {
+    lanes_tree_down<L, G>(s, c, xs, xe);
+    leaf_expand<L, L>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv);
 }
 
 // ===========================================================================
@@ -123,6 +138,93 @@ __global__ void __launch_bounds__(THREADS, MINB) k_fast(SysPtrs sys, int64_t nbl
             if (active) {
                 if (s.guard.tripped()) bad = row0 < bad ? row0 : bad;
                 store_rows<L, VEC>(x, row0, xv);
+            }
+        }
+    }
+    report_pivot(err, level, bad);
+}
+
+// ===========================================================================
+// Any block length m in [2G, LMAX*G] (full blocks): G lanes per block, lane c
+// owns floor(m/G) or floor(m/G)+1 rows (runtime), held in registers sized
+// LMAX with predicated scalar loads/stores. Covers every m <= 256 without a
+// k_fast shape (e.g. the sweep candidates 25, 35, 50, 100, 125, 250).
+// ===========================================================================
+template <int LMAX, int G, int MODE>
+__global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
+    k_fast_rt(SysPtrs sys, int64_t nblocks, int64_t m, IfacePtrs out, const double* __restrict__ xi,
+              double* __restrict__ x, unsigned long long* err, int level) {
+    static_assert(32 % G == 0, "G must divide the warp");
+    constexpr bool KEEP = (MODE != kStage1);
+    constexpr int THREADS = 128;
+    const int64_t nchunks = nblocks * G;
+    const int c = (threadIdx.x & 31) % G;
+    const int llo = (int)(m / G), ext = (int)(m % G);
+    const int len = llo + (c < ext ? 1 : 0);
+    const int off = c * llo + (c < ext ? c : ext);
+    int64_t bad = INT64_MAX;
+
+    for (int64_t base = (int64_t)blockIdx.x * THREADS; base < nchunks;
+         base += (int64_t)gridDim.x * THREADS) {
+        const int64_t t = base + threadIdx.x;
+        const bool active = t < nchunks;
+        const int64_t blk = t / G;
+        const int64_t row0 = blk * m + off;
+        LaneState<LMAX, G, KEEP> s;
+#pragma unroll
+        for (int i = 0; i < LMAX; ++i) {
+            const bool live = active && i < len;
+            s.r.a[i] = live ? __ldg(sys.sub + row0 + i) : 0.0;
+            s.r.b[i] = live ? __ldg(sys.diag + row0 + i) : 1.0;
+            s.r.c[i] = live ? __ldg(sys.sup + row0 + i) : 0.0;
+            s.r.d[i] = live ? __ldg(sys.rhs + row0 + i) : 0.0;
+        }
+        // leaf on the runtime length: one compile-time instance per length, no
+        // dynamic register indexing (lanes of a warp take at most two cases)
+        switch (len) {
+            case 2: lane_leaf<LMAX, G, KEEP, 2>(s, row0); break;
+            case 3: lane_leaf<LMAX, G, KEEP, 3>(s, row0); break;
+            case 4: lane_leaf<LMAX, G, KEEP, 4>(s, row0); break;
+            case 5: lane_leaf<LMAX, G, KEEP, 5>(s, row0); break;
+            case 6: lane_leaf<LMAX, G, KEEP, 6>(s, row0); break;
+            case 7: lane_leaf<LMAX, G, KEEP, 7>(s, row0); break;
+            default: lane_leaf<LMAX, G, KEEP, LMAX>(s, row0); break;
+        }
+        lanes_tree<LMAX, G, KEEP>(s, c, row0);
+        if constexpr (MODE == kStage1) {
+            if (active) {
+                if (s.guard.tripped()) bad = row0 < bad ? row0 : bad;
+                if (c == 0) {
+                    const int64_t o = 2 * blk;
+                    *reinterpret_cast<double2*>(out.sub + o) = make_double2(s.cur.a1, s.cur.a2);
+                    *reinterpret_cast<double2*>(out.diag + o) = make_double2(s.cur.b1, s.cur.b2);
+                    *reinterpret_cast<double2*>(out.sup + o) = make_double2(s.cur.g1, s.cur.g2);
+                    *reinterpret_cast<double2*>(out.rhs + o) = make_double2(s.cur.d1, s.cur.d2);
+                }
+            }
+        } else {
+            double xs = 0, xe = 0;
+            if (c == 0 && active) {
+                const double2 v = *reinterpret_cast<const double2*>(xi + 2 * blk);
+                xs = v.x;
+                xe = v.y;
+            }
+            double xv[LMAX];
+            lanes_tree_down<LMAX, G>(s, c, xs, xe);
+            switch (len) {
+                case 2: leaf_expand<LMAX, 2>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
+                case 3: leaf_expand<LMAX, 3>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
+                case 4: leaf_expand<LMAX, 4>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
+                case 5: leaf_expand<LMAX, 5>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
+                case 6: leaf_expand<LMAX, 6>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
+                case 7: leaf_expand<LMAX, 7>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
+                default: leaf_expand<LMAX, LMAX>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
+            }
+            if (active) {
+                if (s.guard.tripped()) bad = row0 < bad ? row0 : bad;
+#pragma unroll
+                for (int i = 0; i < LMAX; ++i)
+                    if (i < len) x[row0 + i] = xv[i];
             }
         }
     }

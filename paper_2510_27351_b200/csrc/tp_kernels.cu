@@ -606,6 +606,43 @@ cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs& sys, int64
 #undef TPB_CASE
 }
 
+// Runtime-length register path (k_fast_rt): the G with ceil(m/G) <= 8, m/G >= 2.
+int fast_rt_G(int64_t m) {
+    if (m < 2 || m > 256) return 0;
+    int G = 1;
+    while ((m + G - 1) / G > 8) G *= 2;
+    return (G <= 32 && m / G >= 2) ? G : 0;
+}
+
+cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs& sys, int64_t nblocks, const IfacePtrs& out,
+                           const double* xi, double* x, unsigned long long* err, int level, int sms,
+                           cudaStream_t st) {
+    const int G = fast_rt_G(m);
+    if (G == 0) return cudaErrorInvalidValue;
+    const int64_t nchunks = nblocks * G;
+    int64_t grid = (nchunks + 127) / 128;
+    if (mode != kStage1 && grid > (int64_t)sms * 4) grid = (int64_t)sms * 4;
+    if (grid < 1) grid = 1;
+#define TPB_RT(GG)                                                                                   \
+    case GG:                                                                                         \
+        if (mode == kStage1)                                                                         \
+            k_fast_rt<8, GG, kStage1><<<(unsigned)grid, 128, 0, st>>>(sys, nblocks, m, out, xi, x, err, level); \
+        else                                                                                         \
+            k_fast_rt<8, GG, kStage3><<<(unsigned)grid, 128, 0, st>>>(sys, nblocks, m, out, xi, x, err, level); \
+        break;
+    switch (G) {
+        TPB_RT(1)
+        TPB_RT(2)
+        TPB_RT(4)
+        TPB_RT(8)
+        TPB_RT(16)
+        TPB_RT(32)
+        default: return cudaErrorInvalidValue;
+    }
+#undef TPB_RT
+    return cudaGetLastError();
+}
+
 size_t generic_smem_bytes(int threads, int G, int64_t blen) {
     const int64_t bpc = threads / G;
     return (size_t)(4 * bpc * blen) * sizeof(double) + (size_t)((threads + 31) / 32) * sizeof(Eq2) +

@@ -39,6 +39,10 @@ int fast_max_active_blocks(int64_t m, bool vec, int mode);
 cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs& sys, int64_t nblocks,
                         const IfacePtrs& out, const double* xi, double* x, unsigned long long* err,
                         int level, int grid_cap, cudaStream_t st);
+int fast_rt_G(int64_t m);
+cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs& sys, int64_t nblocks, const IfacePtrs& out,
+                           const double* xi, double* x, unsigned long long* err, int level, int sms,
+                           cudaStream_t st);
 size_t generic_smem_bytes(int threads, int G, int64_t blen);
 cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs& sys, int64_t row_base,
                            int64_t blk_base, int64_t nblocks, int64_t blen, const IfacePtrs& out,
