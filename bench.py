@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-runs", type=int, default=3)
     p.add_argument("--prewarm", type=float, default=0.3, help="seconds of untimed solves before warm-up")
+    p.add_argument("--force-sharded", action="store_true",
+                   help="run the multi-GPU code path (NCCL all-gather) even with one rank")
     return p.parse_args()
 
 
@@ -208,7 +210,8 @@ def run_ours(args):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    sharded_mode = world > 1 or args.force_sharded
+    if sharded_mode:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_per = int(args.n)
@@ -222,7 +225,7 @@ def run_ours(args):
     x = torch.empty(n_loc, dtype=torch.float64, device="cuda")
     sys4 = [sys_d.sub, sys_d.diag, sys_d.super, sys_d.rhs]
 
-    if world == 1:
+    if not sharded_mode:
         def step():
             tp.solve_partition_async(sys_d, policy, out=x)
     else:
@@ -255,7 +258,7 @@ def run_ours(args):
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
-    launches_per_step = ctx.last_launch_count()
+    launches_per_step = solver.backend.launches if sharded_mode else ctx.last_launch_count()
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -274,7 +277,7 @@ def run_ours(args):
 
     # per-kernel durations (CUDA events on the launch stream, same inputs)
     prof = {}
-    if world == 1:
+    if not sharded_mode:
         import ctypes as C
         from paper_2510_27351_b200._lib import TpError, lib
         sz = np.asarray(policy.sizes, dtype=np.int64)
@@ -303,7 +306,7 @@ def run_ours(args):
     if args.e2e_steps > 0:
         host = [t.cpu().pin_memory() for t in sys4]
         hx = torch.empty(n_loc, dtype=torch.float64).pin_memory()
-        if world == 1:
+        if not sharded_mode:
             hs = tp.TridiagonalSystem(*(t.numpy() for t in host))
             xo = hx.numpy()
             import ctypes as C
@@ -340,7 +343,7 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
                "ms_per_step": dt / args.e2e_steps * 1e3,
                "path": "tp_solve_partition_f64 (C-ABI host-pointer entry of solve_partition), pinned host buffers"
-               if world == 1 else "pinned host -> device copy, ShardedSolver.solve, device -> pinned host"}
+               if not sharded_mode else "pinned host -> device copy, ShardedSolver.solve, device -> pinned host"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -362,7 +365,10 @@ def run_ours(args):
             if os.path.exists(summ):
                 try:
                     with open(summ) as f:
-                        traffic = json.load(f).get(k, {}).get("dram_bytes")
+                        sd = json.load(f)
+                    # only a capture of this very workload describes this launch
+                    if sd.get("meta", {}).get("n") == n_loc and sd.get("meta", {}).get("policy") == policy.sizes:
+                        traffic = sd.get(k, {}).get("dram_bytes")
                 except Exception:
                     traffic = None
             roof = {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -379,7 +385,7 @@ def run_ours(args):
             "config": {"workload": "recursive partition solve, kNN policy, N=1e8 per GPU (config 3)",
                        "n_per_gpu": n_per, "n_global": n_glob, "policy": policy.sizes,
                        "l2": "inputs 3.2 GB/GPU >> 126 MB L2 (no flush)",
-                       "parallelism": "single GPU" if world == 1 else f"{world} contiguous shards + NCCL all-gather"},
+                       "parallelism": "single GPU" if not sharded_mode else f"{world} contiguous shard(s) + NCCL all-gather"},
             "hbm": {"solve_GBps_40B_per_gpu": solve_gbs,
                     "frac_40B": solve_gbs / peak,
                     "frac_72B": solve_gbs * TWO_PASS_BYTES_PER_UNKNOWN / ALG_BYTES_PER_UNKNOWN / peak,

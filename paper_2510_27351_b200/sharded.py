@@ -50,6 +50,7 @@ class DeviceBackend:
 
     def __init__(self, ctx=None):
         self.ctx = ctx or context()
+        self.launches = 0  # kernels of the last reduce + finish pair
 
     @staticmethod
     def _ptrs(sys4):
@@ -64,6 +65,7 @@ class DeviceBackend:
         _call(lib.tp_shard_reduce_f64_dev, self.ctx.handle, *self._ptrs(sys4), int(sys4[0].numel()),
               sz.ctypes.data_as(C.POINTER(C.c_int64)), len(sz), C.c_void_p(eq8.data_ptr()),
               C.c_void_p(stream))
+        self._reduce_launches = self.ctx.last_launch_count()
         return eq8
 
     def finish(self, sys4, policy, gathered, nranks: int, rank: int, out=None):
@@ -75,6 +77,7 @@ class DeviceBackend:
         _call(lib.tp_shard_finish_f64_dev, self.ctx.handle, *self._ptrs(sys4), int(sys4[0].numel()),
               sz.ctypes.data_as(C.POINTER(C.c_int64)), len(sz), C.c_void_p(gathered.data_ptr()),
               int(nranks), int(rank), C.c_void_p(x.data_ptr()), C.c_void_p(stream))
+        self.launches = getattr(self, "_reduce_launches", 0) + self.ctx.last_launch_count()
         return x
 
     def check(self):

@@ -8,6 +8,8 @@ Parity gates:
   max |dx_i| / max(|x_oracle_i|, 1e-6)         <= 1e-10   (floored elementwise)
   residual_inf(sys, x)                         <= 1e-12   (tridiagonal.hpp:74-87)
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -278,3 +280,41 @@ def test_reciprocal_is_within_one_ulp(tp):
     assert lib.tp_diag_rcp_ulp(10_000_000, 7, C.byref(worst)) == 0
     assert worst.value <= 1, worst.value
 
+
+
+@pytest.mark.skipif(os.environ.get("TPB_SLOW") != "1", reason="set TPB_SLOW=1 (needs ~130 GB host RAM)")
+def test_config4_n1e9_against_the_reference_itself(tp, oracle_mod):
+    """Config 4 at full size: the reference's own generator and solver
+    (oracle/_ref) at N = 1e9 with the kNN policy of the global N, against the
+    single-GPU solve and the 8-rank sharded algorithm (simulated ranks)."""
+    import json
+    import time
+
+    from paper_2510_27351_b200 import sharded
+
+    n = 1_000_000_000
+    pol = tp.predicted_policy(n)
+    assert pol.sizes == [64, 10, 32, 32]
+    t0 = time.time()
+    s = oracle_mod.generate_system(n, 1, impl="ref")
+    t_gen = time.time() - t0
+    t0 = time.time()
+    ref = oracle_mod.solve_partition(s, pol.sizes, impl="ref")
+    t_ref = time.time() - t0
+    x = tp.solve_partition(_sys(tp, s), pol)
+    out = {"n": n, "policy": pol.sizes, "ref_generate_s": t_gen, "ref_solve_s": t_ref,
+           "single_gpu": {"rel_inf_diff": oracle_mod.rel_inf_diff(x, ref),
+                          "floored_rel": oracle_mod.floored_rel_diff(x, ref),
+                          "residual": oracle_mod.residual_inf(s, x)}}
+    del x
+    xs = sharded.simulate_ranks(s.sub, s.diag, s.sup, s.rhs, 8, pol.sizes)
+    out["sharded_8_ranks"] = {"rel_inf_diff": oracle_mod.rel_inf_diff(xs, ref),
+                              "floored_rel": oracle_mod.floored_rel_diff(xs, ref),
+                              "residual": oracle_mod.residual_inf(s, xs)}
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/parity_n1e9.json", "w") as f:
+        json.dump(out, f, indent=1)
+    for k in ("single_gpu", "sharded_8_ranks"):
+        assert out[k]["rel_inf_diff"] <= TOL_NORM
+        assert out[k]["floored_rel"] <= TOL_FLOOR
+        assert out[k]["residual"] <= TOL_RES
