@@ -95,6 +95,27 @@ tp_status tp_solve_partition_observe_f64(tp_ctx* ctx, const double* sub, const d
                                          const int64_t* sizes, int32_t nsizes, double* x,
                                          tp_interface_cb cb, void* user, tp_error* err);
 
+/* FP32: solve_partition<float> / thomas_solve<float> (the reference templates
+ * on Real, partition.hpp:61-77; test_partition.cpp:206-223). Same contracts. */
+typedef void (*tp_interface_cb_f32)(int64_t level, int64_t n, const float* sub, const float* diag,
+                                    const float* super, const float* rhs, void* user);
+tp_status tp_solve_partition_f32(tp_ctx* ctx, const float* sub, const float* diag,
+                                 const float* super, const float* rhs, int64_t n,
+                                 const int64_t* sizes, int32_t nsizes, float* x, tp_error* err);
+tp_status tp_solve_partition_f32_dev(tp_ctx* ctx, const float* sub, const float* diag,
+                                     const float* super, const float* rhs, int64_t n,
+                                     const int64_t* sizes, int32_t nsizes, float* x, void* stream,
+                                     tp_error* err);
+tp_status tp_solve_partition_observe_f32(tp_ctx* ctx, const float* sub, const float* diag,
+                                         const float* super, const float* rhs, int64_t n,
+                                         const int64_t* sizes, int32_t nsizes, float* x,
+                                         tp_interface_cb_f32 cb, void* user, tp_error* err);
+tp_status tp_thomas_solve_f32(tp_ctx* ctx, const float* sub, const float* diag, const float* super,
+                              const float* rhs, int64_t n, float* x, tp_error* err);
+tp_status tp_residual_inf_f32_dev(tp_ctx* ctx, const float* sub, const float* diag,
+                                  const float* super, const float* rhs, int64_t n, const float* x,
+                                  double* out, tp_error* err);
+
 /* thomas_solve(sys) — tridiagonal.hpp:52-72. Same solution, computed by the
  * device finishing solver (exact parallel elimination, not a sequential sweep). */
 tp_status tp_thomas_solve_f64(tp_ctx* ctx, const double* sub, const double* diag,
@@ -131,6 +152,9 @@ tp_status tp_shard_finish_f64_dev(tp_ctx* ctx, const double* sub, const double* 
 tp_status tp_generate_system_f64_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global,
                                      uint64_t seed, double delta, double* sub, double* diag,
                                      double* super, double* rhs, void* stream, tp_error* err);
+tp_status tp_generate_system_f32_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global,
+                                     uint64_t seed, double delta, float* sub, float* diag,
+                                     float* super, float* rhs, void* stream, tp_error* err);
 
 /* ------------------------------------------------------- plan / profile */
 /* make_plan(n, m) — partition.hpp:30-49. bounds (optional) gets K+1 entries. */
@@ -167,7 +191,8 @@ tp_status tp_recursion_sizes(int64_t n, int32_t depth, const int64_t* pairs_n,
                              const int32_t* pairs_label, int64_t npairs, int32_t k,
                              int64_t* sizes /* >= 5 */, int32_t* nsizes, tp_error* err);
 /* The bundled models: which = 0 -> fit_knn(Table I FP64 corrected, k=1),
- * which = 1 -> fit_depth_model(Table II) (test_policy.cpp:14-21). */
+ * which = 1 -> fit_depth_model(Table II) (test_policy.cpp:14-21),
+ * which = 2 -> fit_knn(Table IV FP32 corrected, k=1). */
 tp_status tp_default_model(int32_t which, int64_t* pairs_n, int32_t* pairs_label, int64_t cap,
                            int64_t* npairs, int32_t* k, tp_error* err);
 

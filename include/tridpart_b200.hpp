@@ -13,8 +13,7 @@
 //   TrainingPair / HeuristicModel / fit_knn / predict    knn.hpp:18-77
 //   kMaxRecursionDepth / fit_depth_model / recursion_sizes policy.hpp:11-45
 //   Error hierarchy                                      errors.hpp:7-96
-// Only double precision runs on the device (the reference templates also
-// allow float; the FP32 path is a "next" row).
+// Real = double or float, as the reference's templates (FP32 entries *_f32).
 #pragma once
 
 #include <cstddef>
@@ -23,6 +22,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "tridpart_b200.h"
@@ -117,33 +117,54 @@ struct TridiagonalSystem {
 };
 using Tridiagonal = TridiagonalSystem<double>;
 
-inline std::vector<double> thomas_solve(const Tridiagonal& sys) {
-    std::vector<double> x(sys.size());
+// The device entry points per element type (double: *_f64, float: *_f32).
+namespace b200 {
+template <class Real>
+struct Entry;
+template <>
+struct Entry<double> {
+    static constexpr auto solve = tp_solve_partition_f64;
+    static constexpr auto observe = tp_solve_partition_observe_f64;
+    static constexpr auto thomas = tp_thomas_solve_f64;
+};
+template <>
+struct Entry<float> {
+    static constexpr auto solve = tp_solve_partition_f32;
+    static constexpr auto observe = tp_solve_partition_observe_f32;
+    static constexpr auto thomas = tp_thomas_solve_f32;
+};
+}  // namespace b200
+
+template <class Real>
+std::vector<Real> thomas_solve(const TridiagonalSystem<Real>& sys) {
+    std::vector<Real> x(sys.size());
     tp_error e{};
-    b200::throw_on(tp_thomas_solve_f64(b200::thread_context().get(), sys.sub.data(), sys.diag.data(),
-                                       sys.super.data(), sys.rhs.data(), (int64_t)sys.size(),
-                                       x.data(), &e),
+    b200::throw_on(b200::Entry<Real>::thomas(b200::thread_context().get(), sys.sub.data(),
+                                              sys.diag.data(), sys.super.data(), sys.rhs.data(),
+                                              (int64_t)sys.size(), x.data(), &e),
                    e);
     return x;
 }
 
 // Host-side verification metric, same formula as tridiagonal.hpp:74-87.
-inline double residual_inf(const Tridiagonal& sys, std::span<const double> x) {
+template <class Real>
+Real residual_inf(const TridiagonalSystem<Real>& sys, std::span<const Real> x) {
     const std::size_t n = sys.size();
-    double num = 0, den = 1;
+    Real num = 0, den = 1;
     for (std::size_t i = 0; i < n; ++i) {
-        double ax = sys.diag[i] * x[i];
+        Real ax = sys.diag[i] * x[i];
         if (i > 0) ax += sys.sub[i] * x[i - 1];
         if (i + 1 < n) ax += sys.super[i] * x[i + 1];
-        const double r = ax > sys.rhs[i] ? ax - sys.rhs[i] : sys.rhs[i] - ax;
-        const double d = sys.rhs[i] < 0 ? -sys.rhs[i] : sys.rhs[i];
+        const Real r = ax > sys.rhs[i] ? ax - sys.rhs[i] : sys.rhs[i] - ax;
+        const Real d = sys.rhs[i] < 0 ? -sys.rhs[i] : sys.rhs[i];
         num = r > num ? r : num;
         den = d > den ? d : den;
     }
     return num / den;
 }
-inline double residual_inf(const Tridiagonal& sys, const std::vector<double>& x) {
-    return residual_inf(sys, std::span<const double>(x));
+template <class Real>
+Real residual_inf(const TridiagonalSystem<Real>& sys, const std::vector<Real>& x) {
+    return residual_inf(sys, std::span<const Real>(x));
 }
 
 // ------------------------------------------------------------ partition.hpp
@@ -182,41 +203,43 @@ namespace b200 {
 inline std::vector<int64_t> policy_array(const RecursionPolicy& p) {
     return std::vector<int64_t>(p.sizes.begin(), p.sizes.end());
 }
-template <class F>
-void trampoline(int64_t level, int64_t n, const double* a, const double* b, const double* c,
-                const double* d, void* user) {
-    Tridiagonal t;
+template <class Real, class F>
+void trampoline(int64_t level, int64_t n, const Real* a, const Real* b, const Real* c, const Real* d,
+                void* user) {
+    TridiagonalSystem<Real> t;
     t.sub.assign(a, a + n);
     t.diag.assign(b, b + n);
     t.super.assign(c, c + n);
     t.rhs.assign(d, d + n);
-    (*static_cast<F*>(user))(static_cast<const Tridiagonal&>(t), (std::size_t)level);
+    (*static_cast<F*>(user))(static_cast<const TridiagonalSystem<Real>&>(t), (std::size_t)level);
 }
 }  // namespace b200
 
-template <class InterfaceObserver>
-std::vector<double> solve_partition(const Tridiagonal& sys, const RecursionPolicy& policy,
-                                    InterfaceObserver&& on_interface) {
+template <class Real, class InterfaceObserver>
+std::vector<Real> solve_partition(const TridiagonalSystem<Real>& sys, const RecursionPolicy& policy,
+                                  InterfaceObserver&& on_interface) {
     const auto sz = b200::policy_array(policy);
-    std::vector<double> x(sys.size());
+    std::vector<Real> x(sys.size());
     tp_error e{};
     using F = std::remove_reference_t<InterfaceObserver>;
-    b200::throw_on(tp_solve_partition_observe_f64(
-                       b200::thread_context().get(), sys.sub.data(), sys.diag.data(), sys.super.data(),
-                       sys.rhs.data(), (int64_t)sys.size(), sz.data(), (int32_t)sz.size(), x.data(),
-                       &b200::trampoline<F>, (void*)&on_interface, &e),
+    b200::throw_on(b200::Entry<Real>::observe(b200::thread_context().get(), sys.sub.data(),
+                                               sys.diag.data(), sys.super.data(), sys.rhs.data(),
+                                               (int64_t)sys.size(), sz.data(), (int32_t)sz.size(),
+                                               x.data(), &b200::trampoline<Real, F>,
+                                               (void*)&on_interface, &e),
                    e);
     return x;
 }
 
-inline std::vector<double> solve_partition(const Tridiagonal& sys, const RecursionPolicy& policy) {
+template <class Real>
+std::vector<Real> solve_partition(const TridiagonalSystem<Real>& sys, const RecursionPolicy& policy) {
     const auto sz = b200::policy_array(policy);
-    std::vector<double> x(sys.size());
+    std::vector<Real> x(sys.size());
     tp_error e{};
-    b200::throw_on(tp_solve_partition_f64(b200::thread_context().get(), sys.sub.data(),
-                                          sys.diag.data(), sys.super.data(), sys.rhs.data(),
-                                          (int64_t)sys.size(), sz.data(), (int32_t)sz.size(),
-                                          x.data(), &e),
+    b200::throw_on(b200::Entry<Real>::solve(b200::thread_context().get(), sys.sub.data(),
+                                             sys.diag.data(), sys.super.data(), sys.rhs.data(),
+                                             (int64_t)sys.size(), sz.data(), (int32_t)sz.size(),
+                                             x.data(), &e),
                    e);
     return x;
 }
@@ -289,8 +312,10 @@ inline RecursionPolicy recursion_sizes(std::int64_t n, int depth, const Heuristi
     return p;
 }
 
-// The models the reference's tests fit (test_policy.cpp:14-21), bundled.
+// The models the reference's tests fit (test_policy.cpp:14-21), bundled;
+// default_fp32_size_model: Table IV (FP32) with corrected labels.
 inline HeuristicModel default_size_model() { return b200::bundled(0); }
+inline HeuristicModel default_fp32_size_model() { return b200::bundled(2); }
 inline HeuristicModel default_depth_model() { return b200::bundled(1); }
 
 }  // namespace tridpart

@@ -122,6 +122,11 @@ def ref():
         lib.ref_model_pairs.argtypes = [C.c_int32, _I64, _I32, C.c_int32]
         lib.ref_hardware_concurrency.restype = C.c_uint32
         lib.ref_hardware_concurrency.argtypes = []
+        _F = C.POINTER(C.c_float)
+        lib.ref_solve_partition_f32.restype = C.c_int64
+        lib.ref_solve_partition_f32.argtypes = [C.c_int64, _F, _F, _F, _F, _I64, C.c_int32, _F]
+        lib.ref_residual_inf_f32.restype = C.c_float
+        lib.ref_residual_inf_f32.argtypes = [C.c_int64, _F, _F, _F, _F, _F]
         if lib.ref_load_models(REF_DATA.encode()) != -1:
             raise RuntimeError(f"reference models failed to load from {REF_DATA}")
         _ref = lib
@@ -191,6 +196,25 @@ def solve_partition(sys: System, sizes: Sequence[int], impl: str = "port",
                                        _dp(x), cb, None)
     _status(st)
     return x
+
+
+def solve_partition_f32(sub, diag, sup, rhs, sizes) -> np.ndarray:
+    """The reference's solve_partition<float> (oracle/_ref)."""
+    arrs = [np.ascontiguousarray(a, dtype=np.float32) for a in (sub, diag, sup, rhs)]
+    n = len(arrs[1])
+    x = np.empty(n, dtype=np.float32)
+    sz = np.asarray(sizes, dtype=np.int64)
+    F = C.POINTER(C.c_float)
+    _status(ref().ref_solve_partition_f32(n, *[a.ctypes.data_as(F) for a in arrs],
+                                          sz.ctypes.data_as(_I64), len(sz), x.ctypes.data_as(F)))
+    return x
+
+
+def residual_inf_f32(sub, diag, sup, rhs, x) -> float:
+    """The reference's residual_inf<float> (oracle/_ref)."""
+    arrs = [np.ascontiguousarray(a, dtype=np.float32) for a in (sub, diag, sup, rhs, x)]
+    F = C.POINTER(C.c_float)
+    return float(ref().ref_residual_inf_f32(len(arrs[1]), *[a.ctypes.data_as(F) for a in arrs]))
 
 
 def thomas_solve(sys: System, impl: str = "port") -> np.ndarray:

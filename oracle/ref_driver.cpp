@@ -181,4 +181,32 @@ int32_t ref_model_pairs(int32_t which, int64_t* n, int32_t* label, int32_t cap) 
 }
 
 uint32_t ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
+
+// solve_partition<float> / thomas_solve<float> / residual_inf<float>: the
+// reference's templates instantiated on float (partition.hpp:61-77,
+// test_partition.cpp:206-223).
+int64_t ref_solve_partition_f32(int64_t n, const float* a, const float* b, const float* c,
+                                const float* d, const int64_t* sizes, int32_t nsizes, float* x) {
+    return guarded([&] {
+        TridiagonalSystem<float> s;
+        s.sub.assign(a, a + n);
+        s.diag.assign(b, b + n);
+        s.super.assign(c, c + n);
+        s.rhs.assign(d, d + n);
+        RecursionPolicy p;
+        for (int i = 0; i < nsizes; ++i) p.sizes.push_back((std::size_t)sizes[i]);
+        const auto r = solve_partition(s, p);
+        std::memcpy(x, r.data(), n * sizeof(float));
+    });
+}
+
+float ref_residual_inf_f32(int64_t n, const float* a, const float* b, const float* c, const float* d,
+                           const float* x) {
+    TridiagonalSystem<float> s;
+    s.sub.assign(a, a + n);
+    s.diag.assign(b, b + n);
+    s.super.assign(c, c + n);
+    s.rhs.assign(d, d + n);
+    return residual_inf(s, std::span<const float>(x, (std::size_t)n));
+}
 }

@@ -26,6 +26,8 @@ class TpObservation(C.Structure):
 
 
 INTERFACE_CB = C.CFUNCTYPE(None, C.c_int64, C.c_int64, _D, _D, _D, _D, C.c_void_p)
+_F = C.POINTER(C.c_float)
+INTERFACE_CB_F32 = C.CFUNCTYPE(None, C.c_int64, C.c_int64, _F, _F, _F, _F, C.c_void_p)
 
 # tp_status
 OK, ZERO_PIVOT, INVALID_SIZE, DEPTH_OUT_OF_RANGE, EMPTY_TRAINING_SET, K_TOO_LARGE = 0, 1, 2, 3, 4, 5
@@ -38,7 +40,9 @@ EXPORTS = [
     "tp_residual_inf_f64_dev", "tp_shard_reduce_f64_dev", "tp_shard_finish_f64_dev",
     "tp_generate_system_f64_dev", "tp_make_plan", "tp_plan_levels", "tp_solve_profile_f64_dev",
     "tp_predict", "tp_fit_knn", "tp_recursion_sizes", "tp_default_model", "tp_obs_read",
-    "tp_obs_get", "tp_obs_free", "tp_diag_rcp_ulp",
+    "tp_obs_get", "tp_obs_free", "tp_diag_rcp_ulp", "tp_solve_partition_f32",
+    "tp_solve_partition_f32_dev", "tp_solve_partition_observe_f32", "tp_thomas_solve_f32",
+    "tp_residual_inf_f32_dev", "tp_generate_system_f32_dev",
 ]
 
 
@@ -83,6 +87,15 @@ def _load():
         "tp_obs_get": (C.c_int, [vp, C.c_int64, C.POINTER(TpObservation), _I32, _D, E]),
         "tp_obs_free": (None, [vp]),
         "tp_diag_rcp_ulp": (C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_uint64)]),
+        "tp_solve_partition_f32": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp, E]),
+        "tp_solve_partition_f32_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
+                                                 vp, E]),
+        "tp_solve_partition_observe_f32": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32,
+                                                     vp, INTERFACE_CB_F32, vp, E]),
+        "tp_thomas_solve_f32": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, E]),
+        "tp_residual_inf_f32_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, _D, E]),
+        "tp_generate_system_f32_dev": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
+                                                 C.c_double, vp, vp, vp, vp, vp, E]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -1,14 +1,15 @@
 // C-ABI layer: context, level planner, CUDA-graph cache and the entry points
-// declared in include/tridpart_b200.h.
+// declared in include/tridpart_b200.h (FP64 and FP32, as the reference's
+// solve_partition<Real> template).
 //
 // The planner restates detail::solve_partition_level (partition.hpp:191-224):
 //   level l with n_l < 4            -> finishing solve of that system      (:197)
 //   else make_plan(n_l, sizes[l])   -> Stage 1, interface of 2*K_l rows    (:199-205)
 //   l == depth                      -> finishing solve of the interface    (:208-211)
 //   Stage 3 back up every level                                           (:213-222)
-// The finishing solve runs on the device (single CTA, k_generic<kSolve>); a
-// final system larger than kFinalCap first gets extra device-internal
-// partition levels (m = 32). Those do not change the policy, only how the
+// The finishing solve runs on the device (single CTA, k_final); a final
+// system larger than kFinalCap first gets extra device-internal partition
+// levels (m = 32). Those do not change the policy, only how the
 // thomas_solve(iface) of the reference is computed.
 #include <cuda_runtime.h>
 
@@ -52,6 +53,14 @@ void clear_err(tp_error* err) {
         }                                                                                  \
     } while (0)
 
+#define TP_NEED_CTX(ctx)                                          \
+    do {                                                          \
+        if (!(ctx)) {                                             \
+            set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL"); \
+            return TP_ERR_INVALID_ARGUMENT;                       \
+        }                                                         \
+    } while (0)
+
 // make_plan — partition.hpp:30-49 (block count only).
 int64_t plan_blocks(int64_t n, int64_t m) {
     if (m >= n) return 1;
@@ -60,6 +69,7 @@ int64_t plan_blocks(int64_t n, int64_t m) {
     return leading + 1;
 }
 
+template <class T>
 struct Level {
     int64_t n = 0;      // rows of this level's system
     int64_t m = 0;      // requested block size
@@ -68,30 +78,32 @@ struct Level {
     int64_t tail = 0;   // length of the final block when != m (0 = none)
     bool internal = false;
     // bound pointers
-    SysPtrs in{};
-    double* x_out = nullptr;  // solution of this level's system
-    IfacePtrs iface{};        // next level's system (2K rows)
-    double* x_iface = nullptr;
+    SysPtrs<T> in{};
+    T* x_out = nullptr;    // solution of this level's system
+    IfacePtrs<T> iface{};  // next level's system (2K rows)
+    T* x_iface = nullptr;
 };
 
+template <class T>
 struct Plan {
-    std::vector<Level> levels;
+    std::vector<Level<T>> levels;
     int64_t n_final = 0;
-    SysPtrs final_in{};
-    double* final_x = nullptr;
-    size_t ws_doubles = 0;
+    SysPtrs<T> final_in{};
+    T* final_x = nullptr;
+    size_t ws_elems = 0;  // workspace, in elements of T
 };
 
 inline size_t pad32(size_t v) { return (v + 31) & ~size_t(31); }
 
-bool build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan& p) {
+template <class T>
+void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p) {
     p.levels.clear();
     int64_t cur = n;
     int lvl = 0;
     size_t ws = 0;
     while (nsizes > 0) {
         if (cur < 4) break;
-        Level L;
+        Level<T> L;
         L.n = cur;
         L.m = sizes[lvl];
         L.K = plan_blocks(cur, L.m);
@@ -114,7 +126,7 @@ bool build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan& p) {
     }
     // device-internal levels so the finishing solve fits one CTA
     while (cur > tpb::kFinalCap) {
-        Level L;
+        Level<T> L;
         L.n = cur;
         L.m = kInternalM;
         L.K = plan_blocks(cur, L.m);
@@ -127,14 +139,14 @@ bool build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan& p) {
         cur = 2 * L.K;
     }
     p.n_final = cur;
-    p.ws_doubles = ws;
-    return true;
+    p.ws_elems = ws;
 }
 
-void bind_plan(Plan& p, const SysPtrs& sys, double* x, double* ws) {
-    SysPtrs in = sys;
-    double* xo = x;
-    double* w = ws;
+template <class T>
+void bind_plan(Plan<T>& p, const SysPtrs<T>& sys, T* x, void* ws) {
+    SysPtrs<T> in = sys;
+    T* xo = x;
+    T* w = static_cast<T*>(ws);
     for (auto& L : p.levels) {
         L.in = in;
         L.x_out = xo;
@@ -145,7 +157,7 @@ void bind_plan(Plan& p, const SysPtrs& sys, double* x, double* ws) {
         L.iface.rhs = w + 3 * k2;
         L.x_iface = w + 4 * k2;
         w += 5 * k2;
-        in = SysPtrs{L.iface.sub, L.iface.diag, L.iface.sup, L.iface.rhs};
+        in = SysPtrs<T>{L.iface.sub, L.iface.diag, L.iface.sup, L.iface.rhs};
         xo = L.x_iface;
     }
     p.final_in = in;
@@ -172,14 +184,14 @@ struct tp_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t stream = nullptr;
     bool graphs = true;
-    double* ws = nullptr;
-    size_t ws_cap = 0;  // doubles
+    void* ws = nullptr;  // level workspace
+    size_t ws_cap = 0;   // bytes
     unsigned long long* d_err = nullptr;
     unsigned long long* h_err = nullptr;
     unsigned long long* d_red = nullptr;  // residual / scratch words
-    double* d_small = nullptr;            // shard scratch (x2 + gather scratch)
-    double* dsys = nullptr;               // host-path staging (5 arrays)
-    size_t dsys_cap = 0;                  // rows
+    void* d_small = nullptr;              // shard scratch (x2 + gather scratch)
+    void* dsys = nullptr;                 // host-path staging (5 arrays)
+    size_t dsys_cap = 0;                  // bytes
     int64_t last_launches = 0;
     std::vector<std::pair<int64_t, int>> occ;  // (key, grid cap)
     struct GraphEntry {
@@ -194,11 +206,12 @@ struct tp_ctx {
 
 namespace {
 
+template <class T>
 int fast_grid_cap(tp_ctx* ctx, int64_t m, bool vec, int mode) {
-    const int64_t key = (m << 2) | (vec ? 2 : 0) | mode;
+    const int64_t key = (m << 4) | ((int64_t)sizeof(T) << 2) | (vec ? 2 : 0) | mode;
     for (auto& kv : ctx->occ)
         if (kv.first == key) return kv.second;
-    int nb = tpb::fast_max_active_blocks(m, vec, mode);
+    int nb = tpb::fast_max_active_blocks<T>(m, vec, mode);
     if (nb < 1) nb = 1;
     const int cap = nb * ctx->sms;
     ctx->occ.push_back({key, cap});
@@ -207,6 +220,7 @@ int fast_grid_cap(tp_ctx* ctx, int64_t m, bool vec, int mode) {
 
 using KernelHook = void (*)(void* user, const char* name);
 
+template <class T>
 struct Runner {
     tp_ctx* ctx;
     cudaStream_t st;
@@ -227,35 +241,35 @@ struct Runner {
         if (e != cudaSuccess && status == cudaSuccess) status = e;
     }
 
-    void main_part(const Level& L, int level, int mode) {
+    void main_part(const Level<T>& L, int level, int mode) {
         const bool s1 = (mode == tpb::kStage1);
         int fl, fg;
         if (tpb::fast_shape(L.m, &fl, &fg)) {
             const bool vec = aligned32(L.in.sub) && aligned32(L.in.diag) && aligned32(L.in.sup) &&
                              aligned32(L.in.rhs) && (s1 || aligned32(L.x_out));
-            check(tpb::launch_fast(L.m, vec, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
-                                   ctx->d_err, level, fast_grid_cap(ctx, L.m, vec, mode), st));
+            check(tpb::launch_fast<T>(L.m, vec, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
+                                      ctx->d_err, level, fast_grid_cap<T>(ctx, L.m, vec, mode), st));
             after(s1 ? "stage1" : "stage3", level);
         } else if (tpb::fast_rt_G(L.m) > 0) {
-            check(tpb::launch_fast_rt(L.m, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out, ctx->d_err,
-                                      level, ctx->sms, st));
+            check(tpb::launch_fast_rt<T>(L.m, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
+                                         ctx->d_err, level, ctx->sms, st));
             after(s1 ? "stage1r" : "stage3r", level);
         } else {
-            const int T = tpb::kGenericThreads;
-            const int G = generic_G(L.m, T);
-            const int64_t bpc = T / G;
+            const int NT = tpb::kGenericThreads;
+            const int G = generic_G(L.m, NT);
+            const int64_t bpc = NT / G;
             int64_t grid = (L.kfull + bpc - 1) / bpc;
             grid = std::min<int64_t>(grid, (int64_t)ctx->sms * 8);
-            check(tpb::launch_generic(mode, T, G, (int)grid, L.in, 0, 0, L.kfull, L.m, L.iface,
-                                      L.x_iface, L.x_out, ctx->d_err, level, st));
+            check(tpb::launch_generic<T>(mode, NT, G, (int)grid, L.in, 0, 0, L.kfull, L.m, L.iface,
+                                         L.x_iface, L.x_out, ctx->d_err, level, st));
             after(s1 ? "stage1g" : "stage3g", level);
         }
     }
-    void tail_part(const Level& L, int level, int mode, cudaStream_t s) {
+    void tail_part(const Level<T>& L, int level, int mode, cudaStream_t s) {
         const int G = generic_G(L.tail, tpb::kGenericThreads);
-        const int T = std::max(32, G);
-        check(tpb::launch_generic(mode, T, G, 1, L.in, L.kfull * L.m, L.kfull, 1, L.tail, L.iface,
-                                  L.x_iface, L.x_out, ctx->d_err, level, s));
+        const int NT = std::max(32, G);
+        check(tpb::launch_generic<T>(mode, NT, G, 1, L.in, L.kfull * L.m, L.kfull, 1, L.tail, L.iface,
+                                     L.x_iface, L.x_out, ctx->d_err, level, s));
         after(mode == tpb::kStage1 ? "stage1t" : "stage3t", level);
     }
 
@@ -263,7 +277,7 @@ struct Runner {
     // when its length != m) is independent of the full blocks, so it runs on a
     // forked stream (a parallel branch of the captured graph) and joins before
     // the next dependent kernel. The instrumented path keeps them serial.
-    void stage(const Level& L, int level, int mode) {
+    void stage(const Level<T>& L, int level, int mode) {
         const bool fork = L.kfull > 0 && L.tail > 0 && hook == nullptr;
         if (fork) {
             check(cudaEventRecord(ctx->ev_fork, st));
@@ -278,54 +292,40 @@ struct Runner {
         if (L.tail > 0) tail_part(L, level, mode, st);
     }
 
-    void final_solve(const Plan& p) {
-        check(tpb::launch_final(tpb::kSolve, p.final_in, p.n_final, IfacePtrs{}, nullptr, p.final_x,
-                                ctx->d_err, (int)p.levels.size(), st));
+    void final_solve(const Plan<T>& p) {
+        check(tpb::launch_final<T>(tpb::kSolve, p.final_in, p.n_final, IfacePtrs<T>{}, nullptr, p.final_x,
+                                   ctx->d_err, (int)p.levels.size(), st));
         after("final", (int)p.levels.size());
     }
 
-    // Whole solve (reset error word, Stage 1 down, finish, Stage 3 up).
-    // k_generic over blocks [blk0, blk0 + nblocks) of length blen of one level.
-    void generic_range(int mode, const Level& L, int64_t blk0, int64_t nblocks, int64_t blen,
-                       int level, cudaStream_t s, const char* name) {
-        if (nblocks <= 0) return;
-        const int G = generic_G(blen, tpb::kGenericThreads);
-        const int T = nblocks == 1 ? std::max(32, G) : tpb::kGenericThreads;
-        const int64_t bpc = T / G;
-        int64_t grid = (nblocks + bpc - 1) / bpc;
-        grid = std::min<int64_t>(grid, (int64_t)ctx->sms * 8);
-        check(tpb::launch_generic(mode, T, G, (int)grid, L.in, blk0 * L.m, blk0, nblocks, blen,
-                                  L.iface, L.x_iface, L.x_out, ctx->d_err, level, s));
-        after(name, level);
-    }
-
-    void solve(const Plan& p) {
+    // Whole solve: reset the error word, Stage 1 down, finish, Stage 3 up.
+    void solve(const Plan<T>& p) {
         check(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
         solve_body(p);
     }
-    void solve_body(const Plan& p) {
+    void solve_body(const Plan<T>& p) {
         for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
         final_solve(p);
         for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
     }
 
     // Sharded halves.
-    void shard_reduce(const Plan& p, double* eq8) {
+    void shard_reduce(const Plan<T>& p, T* eq8) {
         check(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
         for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
-        IfacePtrs o{eq8, eq8 + 2, eq8 + 4, eq8 + 6};
-        check(tpb::launch_final(tpb::kStage1, p.final_in, p.n_final, o, nullptr, nullptr, ctx->d_err,
-                                (int)p.levels.size(), st));
+        IfacePtrs<T> o{eq8, eq8 + 2, eq8 + 4, eq8 + 6};
+        check(tpb::launch_final<T>(tpb::kStage1, p.final_in, p.n_final, o, nullptr, nullptr, ctx->d_err,
+                                   (int)p.levels.size(), st));
         after("shard_reduce", (int)p.levels.size());
     }
-    void shard_finish(const Plan& p, const double* eq_all, int nranks, int rank) {
-        double* x2 = ctx->d_small;
-        double* scratch = ctx->d_small + 32;
-        check(tpb::launch_gather_solve(eq_all, nranks, rank, x2, scratch, ctx->d_err,
-                                       (int)p.levels.size() + 1, st));
+    void shard_finish(const Plan<T>& p, const T* eq_all, int nranks, int rank) {
+        T* x2 = static_cast<T*>(ctx->d_small);
+        T* scratch = x2 + 32;
+        check(tpb::launch_gather_solve<T>(eq_all, nranks, rank, x2, scratch, ctx->d_err,
+                                          (int)p.levels.size() + 1, st));
         after("gather_solve", (int)p.levels.size() + 1);
-        check(tpb::launch_final(tpb::kStage3, p.final_in, p.n_final, IfacePtrs{}, x2, p.final_x,
-                                ctx->d_err, (int)p.levels.size(), st));
+        check(tpb::launch_final<T>(tpb::kStage3, p.final_in, p.n_final, IfacePtrs<T>{}, x2, p.final_x,
+                                   ctx->d_err, (int)p.levels.size(), st));
         after("shard_expand", (int)p.levels.size());
         for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
     }
@@ -349,8 +349,8 @@ tp_status validate_policy(int64_t n, const int64_t* sizes, int32_t nsizes, tp_er
     return TP_OK;
 }
 
-tp_status validate(const double* a, const double* b, const double* c, const double* d, int64_t n,
-                   const int64_t* sizes, int32_t nsizes, const double* x, tp_error* err) {
+tp_status validate(const void* a, const void* b, const void* c, const void* d, int64_t n,
+                   const int64_t* sizes, int32_t nsizes, const void* x, tp_error* err) {
     tp_status s = validate_policy(n, sizes, nsizes, err);
     if (s != TP_OK) return s;
     if (!a || !b || !c || !d || !x) {
@@ -360,17 +360,38 @@ tp_status validate(const double* a, const double* b, const double* c, const doub
     return TP_OK;
 }
 
-tp_status ensure_ws(tp_ctx* ctx, size_t doubles, tp_error* err) {
-    if (doubles <= ctx->ws_cap) return TP_OK;
-    // growing the workspace invalidates every captured graph
+void drop_graphs(tp_ctx* ctx) {
     for (auto& g : ctx->gcache) cudaGraphExecDestroy(g.exec);
     ctx->gcache.clear();
+}
+
+tp_status ensure_ws(tp_ctx* ctx, size_t bytes, tp_error* err) {
+    if (bytes <= ctx->ws_cap) return TP_OK;
+    drop_graphs(ctx);  // growing the workspace invalidates every captured graph
     if (ctx->ws) cudaFree(ctx->ws);
     ctx->ws = nullptr;
     ctx->ws_cap = 0;
-    const size_t want = doubles + doubles / 8 + 1024;
-    TP_CUDA(cudaMalloc(&ctx->ws, want * sizeof(double)));
+    const size_t want = bytes + bytes / 8 + 8192;
+    TP_CUDA(cudaMalloc(&ctx->ws, want));
     ctx->ws_cap = want;
+    return TP_OK;
+}
+
+// host-path staging: five arrays of n elements (sub, diag, super, rhs, x)
+template <class T>
+tp_status ensure_dsys(tp_ctx* ctx, int64_t n, T** arrays, tp_error* err) {
+    const size_t rows = pad32((size_t)n);
+    const size_t bytes = 5 * rows * sizeof(T);
+    if (bytes > ctx->dsys_cap) {
+        drop_graphs(ctx);
+        if (ctx->dsys) cudaFree(ctx->dsys);
+        ctx->dsys = nullptr;
+        ctx->dsys_cap = 0;
+        TP_CUDA(cudaMalloc(&ctx->dsys, bytes));
+        ctx->dsys_cap = bytes;
+    }
+    T* base = static_cast<T*>(ctx->dsys);
+    for (int i = 0; i < 5; ++i) arrays[i] = base + i * rows;
     return TP_OK;
 }
 
@@ -384,11 +405,11 @@ tp_status decode_device_error(tp_ctx* ctx, tp_error* err) {
 }
 
 // Runs `fn(runner)` directly or through a cached CUDA graph keyed by `key`.
-template <class Fn>
+template <class T, class Fn>
 tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_t>& key, Fn&& fn,
                           tp_error* err) {
     if (!ctx->graphs) {
-        Runner r{ctx, st};
+        Runner<T> r{ctx, st};
         fn(r);
         ctx->last_launches = r.launches;
         if (r.status != cudaSuccess) {
@@ -413,7 +434,7 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
         own_cap = true;
     }
     TP_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    Runner r{ctx, cap};
+    Runner<T> r{ctx, cap};
     fn(r);
     cudaGraph_t graph = nullptr;
     cudaError_t ce = cudaStreamEndCapture(cap, &graph);
@@ -450,10 +471,11 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
     return TP_OK;
 }
 
+template <class T>
 std::vector<int64_t> make_key(int64_t tag, int64_t n, const int64_t* sizes, int32_t nsizes,
                               std::initializer_list<const void*> ptrs, int64_t extra = 0) {
     std::vector<int64_t> k;
-    k.push_back(tag);
+    k.push_back(tag * 16 + (int64_t)sizeof(T));
     k.push_back(n);
     k.push_back(extra);
     for (int i = 0; i < nsizes; ++i) k.push_back(sizes[i]);
@@ -466,17 +488,238 @@ cudaStream_t pick_stream(tp_ctx* ctx, void* s) {
     return s ? static_cast<cudaStream_t>(s) : ctx->stream;
 }
 
-tp_status ensure_dsys(tp_ctx* ctx, int64_t n, tp_error* err) {
-    if ((size_t)n <= ctx->dsys_cap) return TP_OK;
-    for (auto& g : ctx->gcache) cudaGraphExecDestroy(g.exec);
-    ctx->gcache.clear();
-    if (ctx->dsys) cudaFree(ctx->dsys);
-    ctx->dsys = nullptr;
-    ctx->dsys_cap = 0;
-    const size_t rows = pad32((size_t)n);
-    TP_CUDA(cudaMalloc(&ctx->dsys, 5 * rows * sizeof(double)));
-    ctx->dsys_cap = rows;
+// ------------------------------------------------------------ implementations
+template <class T>
+tp_status solve_dev(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs, int64_t n,
+                    const int64_t* sizes, int32_t nsizes, T* x, void* stream, tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaSetDevice(ctx->device));
+    Plan<T> p;
+    build_plan(n, sizes, nsizes, p);
+    s = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, x, ctx->ws);
+    const cudaStream_t st = pick_stream(ctx, stream);
+    auto key = make_key<T>(1, n, sizes, nsizes, {sub, diag, super, rhs, x, ctx->ws});
+    return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.solve(p); }, err);
+}
+
+// H2D of the four arrays into the context's staging buffers, `body(device
+// arrays)` on the context stream, D2H of x, synchronise, decode zero pivots.
+template <class T, class Body>
+tp_status host_roundtrip(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs,
+                         int64_t n, T* x, Body&& body, tp_error* err) {
+    T* d[5];
+    tp_status s = ensure_dsys<T>(ctx, n, d, err);
+    if (s != TP_OK) return s;
+    const cudaStream_t st = ctx->stream;
+    const size_t bytes = (size_t)n * sizeof(T);
+    TP_CUDA(cudaMemcpyAsync(d[0], sub, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(d[1], diag, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(d[2], super, bytes, cudaMemcpyHostToDevice, st));
+    TP_CUDA(cudaMemcpyAsync(d[3], rhs, bytes, cudaMemcpyHostToDevice, st));
+    s = body(d, st);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaMemcpyAsync(x, d[4], bytes, cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaStreamSynchronize(st));
+    return decode_device_error(ctx, err);
+}
+
+template <class T>
+tp_status solve_host(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs, int64_t n,
+                     const int64_t* sizes, int32_t nsizes, T* x, tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaSetDevice(ctx->device));
+    return host_roundtrip<T>(ctx, sub, diag, super, rhs, n, x,
+                             [&](T** d, cudaStream_t st) {
+                                 return solve_dev<T>(ctx, d[0], d[1], d[2], d[3], n, sizes, nsizes,
+                                                     d[4], st, err);
+                             },
+                             err);
+}
+
+template <class T>
+tp_status solve_observe(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs,
+                        int64_t n, const int64_t* sizes, int32_t nsizes, T* x,
+                        void (*emit)(int64_t, int64_t, const T*, const T*, const T*, const T*, void*),
+                        void* user, tp_error* err) {
+    tp_status s = solve_host<T>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    if (s != TP_OK || emit == nullptr) return s;
+    T* d[5];
+    s = ensure_dsys<T>(ctx, n, d, err);  // same buffers the solve used
+    if (s != TP_OK) return s;
+    Plan<T> p;
+    build_plan(n, sizes, nsizes, p);
+    bind_plan(p, SysPtrs<T>{d[0], d[1], d[2], d[3]}, d[4], ctx->ws);
+    std::vector<T> h;
+    for (size_t l = 0; l < p.levels.size(); ++l) {
+        const Level<T>& L = p.levels[l];
+        if (L.internal) break;  // device-internal levels are not part of the policy
+        const int64_t n2 = 2 * L.K;
+        h.resize((size_t)(4 * n2));
+        TP_CUDA(cudaMemcpy(h.data(), L.iface.sub, n2 * sizeof(T), cudaMemcpyDeviceToHost));
+        TP_CUDA(cudaMemcpy(h.data() + n2, L.iface.diag, n2 * sizeof(T), cudaMemcpyDeviceToHost));
+        TP_CUDA(cudaMemcpy(h.data() + 2 * n2, L.iface.sup, n2 * sizeof(T), cudaMemcpyDeviceToHost));
+        TP_CUDA(cudaMemcpy(h.data() + 3 * n2, L.iface.rhs, n2 * sizeof(T), cudaMemcpyDeviceToHost));
+        emit((int64_t)l, n2, h.data(), h.data() + n2, h.data() + 2 * n2, h.data() + 3 * n2, user);
+    }
     return TP_OK;
+}
+
+// thomas_solve: no policy levels, only device-internal ones (large n) + finish.
+template <class T>
+tp_status thomas_host(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs, int64_t n,
+                      T* x, tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    if (n <= 0) {
+        set_err(err, TP_ERR_INVALID_SIZE, "empty system");
+        return TP_ERR_INVALID_SIZE;
+    }
+    if (!sub || !diag || !super || !rhs || !x) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null array pointer");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    return host_roundtrip<T>(
+        ctx, sub, diag, super, rhs, n, x,
+        [&](T** d, cudaStream_t st) -> tp_status {
+            Plan<T> p;
+            build_plan(n, nullptr, 0, p);
+            tp_status s2 = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
+            if (s2 != TP_OK) return s2;
+            bind_plan(p, SysPtrs<T>{d[0], d[1], d[2], d[3]}, d[4], ctx->ws);
+            auto key = make_key<T>(2, n, nullptr, 0, {d[0], d[1], d[2], d[3], d[4], ctx->ws});
+            return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.solve(p); }, err);
+        },
+        err);
+}
+
+template <class T>
+tp_status residual_dev(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs, int64_t n,
+                       const T* x, double* out, tp_error* err) {
+    clear_err(err);
+    if (!ctx || !out || !sub || !diag || !super || !rhs || !x) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    const cudaStream_t st = ctx->stream;
+    TP_CUDA(cudaMemsetAsync(ctx->d_red, 0, 2 * sizeof(unsigned long long), st));
+    TP_CUDA(tpb::launch_residual<T>(SysPtrs<T>{sub, diag, super, rhs}, n, x, ctx->d_red, ctx->sms, st));
+    unsigned long long h[2];
+    TP_CUDA(cudaMemcpyAsync(h, ctx->d_red, sizeof(h), cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaStreamSynchronize(st));
+    double num, den;
+    std::memcpy(&num, &h[0], sizeof(double));
+    std::memcpy(&den, &h[1], sizeof(double));
+    if (den < 1.0) den = 1.0;
+    *out = num / den;
+    return TP_OK;
+}
+
+template <class T>
+tp_status shard_reduce(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs,
+                       int64_t n_local, const int64_t* sizes, int32_t nsizes, T* eq8_dev, void* stream,
+                       tp_error* err) {
+    clear_err(err);
+    if (!ctx || !eq8_dev) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    tp_status s = validate(sub, diag, super, rhs, n_local, sizes, nsizes, eq8_dev, err);
+    if (s != TP_OK) return s;
+    if (n_local < 2) {
+        set_err(err, TP_ERR_INVALID_SIZE, "a shard needs at least 2 rows");
+        return TP_ERR_INVALID_SIZE;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    Plan<T> p;
+    build_plan(n_local, sizes, nsizes, p);
+    s = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, (T*)nullptr, ctx->ws);
+    const cudaStream_t st = pick_stream(ctx, stream);
+    auto key = make_key<T>(3, n_local, sizes, nsizes, {sub, diag, super, rhs, eq8_dev, ctx->ws});
+    return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.shard_reduce(p, eq8_dev); }, err);
+}
+
+template <class T>
+tp_status shard_finish(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs,
+                       int64_t n_local, const int64_t* sizes, int32_t nsizes, const T* eq_all_dev,
+                       int32_t nranks, int32_t rank, T* x_dev, void* stream, tp_error* err) {
+    clear_err(err);
+    if (!ctx || !eq_all_dev) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    // d_small holds 32 + 4*nranks elements of scratch (4096 bytes)
+    if (nranks < 1 || nranks > 120 || rank < 0 || rank >= nranks) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "bad rank / nranks (1..120 ranks)");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    tp_status s = validate(sub, diag, super, rhs, n_local, sizes, nsizes, x_dev, err);
+    if (s != TP_OK) return s;
+    if (n_local < 2) {
+        set_err(err, TP_ERR_INVALID_SIZE, "a shard needs at least 2 rows");
+        return TP_ERR_INVALID_SIZE;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    Plan<T> p;
+    build_plan(n_local, sizes, nsizes, p);
+    s = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, x_dev, ctx->ws);
+    const cudaStream_t st = pick_stream(ctx, stream);
+    auto key = make_key<T>(4, n_local, sizes, nsizes,
+                           {sub, diag, super, rhs, eq_all_dev, x_dev, ctx->ws},
+                           ((int64_t)nranks << 32) | rank);
+    return run_maybe_graph<T>(ctx, st, key,
+                              [&](Runner<T>& r) { r.shard_finish(p, eq_all_dev, nranks, rank); }, err);
+}
+
+template <class T>
+tp_status generate_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
+                       T* sub, T* diag, T* super, T* rhs, void* stream, tp_error* err) {
+    clear_err(err);
+    if (!ctx || !sub || !diag || !super || !rhs) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    if (n_global < 2 || n < 0 || row0 < 0 || row0 + n > n_global) {  // bench.hpp:69
+        set_err(err, TP_ERR_INVALID_SIZE, "system size must be >= 2");
+        return TP_ERR_INVALID_SIZE;
+    }
+    if (!(delta > 1.0)) {  // bench.hpp:70
+        set_err(err, TP_ERR_INVALID_SIZE, "dominance factor must be > 1");
+        return TP_ERR_INVALID_SIZE;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    TP_CUDA(tpb::launch_generate<T>(n, row0, n_global, seed, delta, sub, diag, super, rhs, ctx->sms,
+                                    pick_stream(ctx, stream)));
+    return TP_OK;
+}
+
+struct ProfileState {
+    cudaStream_t st;
+    std::vector<cudaEvent_t> evs;
+    std::vector<std::string> names;
+};
+
+void profile_hook(void* user, const char* name) {
+    auto* ps = static_cast<ProfileState*>(user);
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, ps->st);
+    ps->evs.push_back(e);
+    ps->names.push_back(name);
 }
 
 }  // namespace
@@ -551,275 +794,113 @@ void tp_ctx_destroy(tp_ctx* ctx) {
 
 tp_status tp_ctx_set_stream(tp_ctx* ctx, void* stream, tp_error* err) {
     clear_err(err);
-    if (!ctx) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
+    TP_NEED_CTX(ctx);
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
     return TP_OK;
 }
 
 tp_status tp_ctx_set_graphs(tp_ctx* ctx, int32_t enabled, tp_error* err) {
     clear_err(err);
-    if (!ctx) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
+    TP_NEED_CTX(ctx);
     ctx->graphs = enabled != 0;
     return TP_OK;
 }
 
 int64_t tp_ctx_last_launch_count(const tp_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
 
-
-tp_status tp_solve_partition_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
-                                     const double* super, const double* rhs, int64_t n,
-                                     const int64_t* sizes, int32_t nsizes, double* x, void* stream,
-                                     tp_error* err) {
-    clear_err(err);
-    if (!ctx) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
-    if (s != TP_OK) return s;
-    TP_CUDA(cudaSetDevice(ctx->device));
-    Plan p;
-    build_plan(n, sizes, nsizes, p);
-    s = ensure_ws(ctx, p.ws_doubles, err);
-    if (s != TP_OK) return s;
-    bind_plan(p, SysPtrs{sub, diag, super, rhs}, x, ctx->ws);
-    const cudaStream_t st = pick_stream(ctx, stream);
-    auto key = make_key(1, n, sizes, nsizes, {sub, diag, super, rhs, x, ctx->ws});
-    return run_maybe_graph(ctx, st, key, [&](Runner& r) { r.solve(p); }, err);
-}
-
 tp_status tp_check_device_error(tp_ctx* ctx, tp_error* err) {
     clear_err(err);
-    if (!ctx) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
+    TP_NEED_CTX(ctx);
     TP_CUDA(cudaMemcpy(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     return decode_device_error(ctx, err);
 }
 
+// ---- solve_partition ------------------------------------------------------
+tp_status tp_solve_partition_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                     const double* super, const double* rhs, int64_t n,
+                                     const int64_t* sizes, int32_t nsizes, double* x, void* stream,
+                                     tp_error* err) {
+    return solve_dev<double>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, stream, err);
+}
+tp_status tp_solve_partition_f32_dev(tp_ctx* ctx, const float* sub, const float* diag,
+                                     const float* super, const float* rhs, int64_t n,
+                                     const int64_t* sizes, int32_t nsizes, float* x, void* stream,
+                                     tp_error* err) {
+    return solve_dev<float>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, stream, err);
+}
 tp_status tp_solve_partition_f64(tp_ctx* ctx, const double* sub, const double* diag,
                                  const double* super, const double* rhs, int64_t n,
                                  const int64_t* sizes, int32_t nsizes, double* x, tp_error* err) {
-    clear_err(err);
-    if (!ctx) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
-    if (s != TP_OK) return s;
-    TP_CUDA(cudaSetDevice(ctx->device));
-    s = ensure_dsys(ctx, n, err);
-    if (s != TP_OK) return s;
-    const size_t rows = ctx->dsys_cap;
-    double* da = ctx->dsys;
-    double* db = da + rows;
-    double* dc = db + rows;
-    double* dd = dc + rows;
-    double* dx = dd + rows;
-    const cudaStream_t st = ctx->stream;
-    const size_t bytes = (size_t)n * sizeof(double);
-    TP_CUDA(cudaMemcpyAsync(da, sub, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(db, diag, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(dc, super, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(dd, rhs, bytes, cudaMemcpyHostToDevice, st));
-    s = tp_solve_partition_f64_dev(ctx, da, db, dc, dd, n, sizes, nsizes, dx, st, err);
-    if (s != TP_OK) return s;
-    TP_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, st));
-    TP_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    TP_CUDA(cudaStreamSynchronize(st));
-    return decode_device_error(ctx, err);
+    return solve_host<double>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, err);
 }
-
+tp_status tp_solve_partition_f32(tp_ctx* ctx, const float* sub, const float* diag,
+                                 const float* super, const float* rhs, int64_t n,
+                                 const int64_t* sizes, int32_t nsizes, float* x, tp_error* err) {
+    return solve_host<float>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, err);
+}
 tp_status tp_solve_partition_observe_f64(tp_ctx* ctx, const double* sub, const double* diag,
                                          const double* super, const double* rhs, int64_t n,
                                          const int64_t* sizes, int32_t nsizes, double* x,
                                          tp_interface_cb cb, void* user, tp_error* err) {
-    tp_status s = tp_solve_partition_f64(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, err);
-    if (s != TP_OK || cb == nullptr) return s;
-    Plan p;
-    build_plan(n, sizes, nsizes, p);
-    bind_plan(p, SysPtrs{ctx->dsys, ctx->dsys + ctx->dsys_cap, ctx->dsys + 2 * ctx->dsys_cap,
-                         ctx->dsys + 3 * ctx->dsys_cap},
-              ctx->dsys + 4 * ctx->dsys_cap, ctx->ws);
-    std::vector<double> h;
-    for (size_t l = 0; l < p.levels.size(); ++l) {
-        const Level& L = p.levels[l];
-        if (L.internal) break;  // device-internal levels are not part of the policy
-        const int64_t n2 = 2 * L.K;
-        h.resize((size_t)(4 * n2));
-        TP_CUDA(cudaMemcpy(h.data(), L.iface.sub, n2 * sizeof(double), cudaMemcpyDeviceToHost));
-        TP_CUDA(cudaMemcpy(h.data() + n2, L.iface.diag, n2 * sizeof(double), cudaMemcpyDeviceToHost));
-        TP_CUDA(cudaMemcpy(h.data() + 2 * n2, L.iface.sup, n2 * sizeof(double), cudaMemcpyDeviceToHost));
-        TP_CUDA(cudaMemcpy(h.data() + 3 * n2, L.iface.rhs, n2 * sizeof(double), cudaMemcpyDeviceToHost));
-        cb((int64_t)l, n2, h.data(), h.data() + n2, h.data() + 2 * n2, h.data() + 3 * n2, user);
-    }
-    return TP_OK;
+    return solve_observe<double>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, cb, user, err);
+}
+tp_status tp_solve_partition_observe_f32(tp_ctx* ctx, const float* sub, const float* diag,
+                                         const float* super, const float* rhs, int64_t n,
+                                         const int64_t* sizes, int32_t nsizes, float* x,
+                                         tp_interface_cb_f32 cb, void* user, tp_error* err) {
+    return solve_observe<float>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, cb, user, err);
 }
 
+// ---- thomas_solve / residual_inf ------------------------------------------
 tp_status tp_thomas_solve_f64(tp_ctx* ctx, const double* sub, const double* diag,
                               const double* super, const double* rhs, int64_t n, double* x,
                               tp_error* err) {
-    // A policy with no partition levels: n >= 4 still needs one level of m >= n
-    // for the reference planner, so drive the finishing solver directly.
-    clear_err(err);
-    if (!ctx) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    if (n <= 0) {
-        set_err(err, TP_ERR_INVALID_SIZE, "empty system");
-        return TP_ERR_INVALID_SIZE;
-    }
-    if (!sub || !diag || !super || !rhs || !x) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "null array pointer");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    TP_CUDA(cudaSetDevice(ctx->device));
-    tp_status s = ensure_dsys(ctx, n, err);
-    if (s != TP_OK) return s;
-    const size_t rows = ctx->dsys_cap;
-    double* da = ctx->dsys;
-    double* db = da + rows;
-    double* dc = db + rows;
-    double* dd = dc + rows;
-    double* dx = dd + rows;
-    const cudaStream_t st = ctx->stream;
-    const size_t bytes = (size_t)n * sizeof(double);
-    TP_CUDA(cudaMemcpyAsync(da, sub, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(db, diag, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(dc, super, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(dd, rhs, bytes, cudaMemcpyHostToDevice, st));
-    // no policy levels: only device-internal levels (if n is large) + finish
-    Plan p;
-    build_plan(n, nullptr, 0, p);
-    s = ensure_ws(ctx, p.ws_doubles, err);
-    if (s != TP_OK) return s;
-    bind_plan(p, SysPtrs{da, db, dc, dd}, dx, ctx->ws);
-    auto key = make_key(2, n, nullptr, 0, {da, db, dc, dd, dx, ctx->ws});
-    s = run_maybe_graph(ctx, st, key, [&](Runner& r) { r.solve(p); }, err);
-    if (s != TP_OK) return s;
-    TP_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, st));
-    TP_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    TP_CUDA(cudaStreamSynchronize(st));
-    return decode_device_error(ctx, err);
+    return thomas_host<double>(ctx, sub, diag, super, rhs, n, x, err);
 }
-
+tp_status tp_thomas_solve_f32(tp_ctx* ctx, const float* sub, const float* diag, const float* super,
+                              const float* rhs, int64_t n, float* x, tp_error* err) {
+    return thomas_host<float>(ctx, sub, diag, super, rhs, n, x, err);
+}
 tp_status tp_residual_inf_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
                                   const double* super, const double* rhs, int64_t n,
                                   const double* x, double* out, tp_error* err) {
-    clear_err(err);
-    if (!ctx || !out || !sub || !diag || !super || !rhs || !x) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    TP_CUDA(cudaSetDevice(ctx->device));
-    const cudaStream_t st = ctx->stream;
-    TP_CUDA(cudaMemsetAsync(ctx->d_red, 0, 2 * sizeof(unsigned long long), st));
-    TP_CUDA(tpb::launch_residual(SysPtrs{sub, diag, super, rhs}, n, x, ctx->d_red, ctx->sms, st));
-    unsigned long long h[2];
-    TP_CUDA(cudaMemcpyAsync(h, ctx->d_red, sizeof(h), cudaMemcpyDeviceToHost, st));
-    TP_CUDA(cudaStreamSynchronize(st));
-    double num, den;
-    std::memcpy(&num, &h[0], sizeof(double));
-    std::memcpy(&den, &h[1], sizeof(double));
-    if (den < 1.0) den = 1.0;
-    *out = num / den;
-    return TP_OK;
+    return residual_dev<double>(ctx, sub, diag, super, rhs, n, x, out, err);
+}
+tp_status tp_residual_inf_f32_dev(tp_ctx* ctx, const float* sub, const float* diag,
+                                  const float* super, const float* rhs, int64_t n, const float* x,
+                                  double* out, tp_error* err) {
+    return residual_dev<float>(ctx, sub, diag, super, rhs, n, x, out, err);
 }
 
+// ---- sharded --------------------------------------------------------------
 tp_status tp_shard_reduce_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
                                   const double* super, const double* rhs, int64_t n_local,
                                   const int64_t* sizes, int32_t nsizes, double* eq8_dev,
                                   void* stream, tp_error* err) {
-    clear_err(err);
-    if (!ctx || !eq8_dev) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    tp_status s = validate(sub, diag, super, rhs, n_local, sizes, nsizes, eq8_dev, err);
-    if (s != TP_OK) return s;
-    if (n_local < 2) {
-        set_err(err, TP_ERR_INVALID_SIZE, "a shard needs at least 2 rows");
-        return TP_ERR_INVALID_SIZE;
-    }
-    TP_CUDA(cudaSetDevice(ctx->device));
-    Plan p;
-    build_plan(n_local, sizes, nsizes, p);
-    s = ensure_ws(ctx, p.ws_doubles, err);
-    if (s != TP_OK) return s;
-    bind_plan(p, SysPtrs{sub, diag, super, rhs}, nullptr, ctx->ws);
-    const cudaStream_t st = pick_stream(ctx, stream);
-    auto key = make_key(3, n_local, sizes, nsizes, {sub, diag, super, rhs, eq8_dev, ctx->ws});
-    return run_maybe_graph(ctx, st, key, [&](Runner& r) { r.shard_reduce(p, eq8_dev); }, err);
+    return shard_reduce<double>(ctx, sub, diag, super, rhs, n_local, sizes, nsizes, eq8_dev, stream, err);
 }
-
 tp_status tp_shard_finish_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
                                   const double* super, const double* rhs, int64_t n_local,
                                   const int64_t* sizes, int32_t nsizes, const double* eq_all_dev,
                                   int32_t nranks, int32_t rank, double* x_dev, void* stream,
                                   tp_error* err) {
-    clear_err(err);
-    if (!ctx || !eq_all_dev) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    if (nranks < 1 || nranks > 1024 || rank < 0 || rank >= nranks) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "bad rank / nranks");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    tp_status s = validate(sub, diag, super, rhs, n_local, sizes, nsizes, x_dev, err);
-    if (s != TP_OK) return s;
-    if (n_local < 2) {
-        set_err(err, TP_ERR_INVALID_SIZE, "a shard needs at least 2 rows");
-        return TP_ERR_INVALID_SIZE;
-    }
-    TP_CUDA(cudaSetDevice(ctx->device));
-    if (4 * nranks + 64 > 512) {
-        // d_small holds 32 + 4*nranks doubles of scratch
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "too many ranks for the scratch buffer");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    Plan p;
-    build_plan(n_local, sizes, nsizes, p);
-    s = ensure_ws(ctx, p.ws_doubles, err);
-    if (s != TP_OK) return s;
-    bind_plan(p, SysPtrs{sub, diag, super, rhs}, x_dev, ctx->ws);
-    const cudaStream_t st = pick_stream(ctx, stream);
-    auto key = make_key(4, n_local, sizes, nsizes, {sub, diag, super, rhs, eq_all_dev, x_dev, ctx->ws},
-                        ((int64_t)nranks << 32) | rank);
-    return run_maybe_graph(ctx, st, key,
-                           [&](Runner& r) { r.shard_finish(p, eq_all_dev, nranks, rank); }, err);
+    return shard_finish<double>(ctx, sub, diag, super, rhs, n_local, sizes, nsizes, eq_all_dev, nranks,
+                                rank, x_dev, stream, err);
 }
 
+// ---- synthetic inputs -----------------------------------------------------
 tp_status tp_generate_system_f64_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global,
                                      uint64_t seed, double delta, double* sub, double* diag,
                                      double* super, double* rhs, void* stream, tp_error* err) {
-    clear_err(err);
-    if (!ctx || !sub || !diag || !super || !rhs) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
-    if (n_global < 2 || n < 0 || row0 < 0 || row0 + n > n_global) {  // bench.hpp:69
-        set_err(err, TP_ERR_INVALID_SIZE, "system size must be >= 2");
-        return TP_ERR_INVALID_SIZE;
-    }
-    if (!(delta > 1.0)) {  // bench.hpp:70
-        set_err(err, TP_ERR_INVALID_SIZE, "dominance factor must be > 1");
-        return TP_ERR_INVALID_SIZE;
-    }
-    TP_CUDA(cudaSetDevice(ctx->device));
-    TP_CUDA(tpb::launch_generate(n, row0, n_global, seed, delta, sub, diag, super, rhs, ctx->sms,
-                                 pick_stream(ctx, stream)));
-    return TP_OK;
+    return generate_dev<double>(ctx, n, row0, n_global, seed, delta, sub, diag, super, rhs, stream, err);
+}
+tp_status tp_generate_system_f32_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global,
+                                     uint64_t seed, double delta, float* sub, float* diag,
+                                     float* super, float* rhs, void* stream, tp_error* err) {
+    return generate_dev<float>(ctx, n, row0, n_global, seed, delta, sub, diag, super, rhs, stream, err);
 }
 
+// ---- plans ----------------------------------------------------------------
 tp_status tp_make_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* nblocks, tp_error* err) {
     clear_err(err);
     if (n < 2) {
@@ -845,7 +926,7 @@ tp_status tp_plan_levels(int64_t n, const int64_t* sizes, int32_t nsizes, int64_
     clear_err(err);
     tp_status s = validate_policy(n, sizes, nsizes, err);
     if (s != TP_OK) return s;
-    Plan p;
+    Plan<double> p;
     build_plan(n, sizes, nsizes, p);
     if ((int32_t)p.levels.size() > max_levels) {
         set_err(err, TP_ERR_INVALID_ARGUMENT, "max_levels too small");
@@ -860,46 +941,29 @@ tp_status tp_plan_levels(int64_t n, const int64_t* sizes, int32_t nsizes, int64_
     return TP_OK;
 }
 
-struct ProfileState {
-    cudaStream_t st;
-    std::vector<cudaEvent_t> evs;
-    std::vector<std::string> names;
-};
-
-static void profile_hook(void* user, const char* name) {
-    auto* ps = static_cast<ProfileState*>(user);
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, ps->st);
-    ps->evs.push_back(e);
-    ps->names.push_back(name);
-}
-
+// ---- instrumented solve ---------------------------------------------------
 tp_status tp_solve_profile_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
                                    const double* super, const double* rhs, int64_t n,
                                    const int64_t* sizes, int32_t nsizes, double* x, float* kernel_ms,
                                    char* names, int32_t max_kernels, int32_t* nkernels,
                                    tp_error* err) {
     clear_err(err);
-    if (!ctx) {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "ctx is NULL");
-        return TP_ERR_INVALID_ARGUMENT;
-    }
+    TP_NEED_CTX(ctx);
     tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
     if (s != TP_OK) return s;
     TP_CUDA(cudaSetDevice(ctx->device));
-    Plan p;
+    Plan<double> p;
     build_plan(n, sizes, nsizes, p);
-    s = ensure_ws(ctx, p.ws_doubles, err);
+    s = ensure_ws(ctx, p.ws_elems * sizeof(double), err);
     if (s != TP_OK) return s;
-    bind_plan(p, SysPtrs{sub, diag, super, rhs}, x, ctx->ws);
+    bind_plan(p, SysPtrs<double>{sub, diag, super, rhs}, x, ctx->ws);
     const cudaStream_t st = ctx->stream;
     ProfileState ps{st, {}, {}};
     cudaEvent_t e0;
     TP_CUDA(cudaEventCreate(&e0));
     TP_CUDA(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
     TP_CUDA(cudaEventRecord(e0, st));
-    Runner r{ctx, st};
+    Runner<double> r{ctx, st};
     r.hook = profile_hook;
     r.hook_user = &ps;
     r.solve_body(p);

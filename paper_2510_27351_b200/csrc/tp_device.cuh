@@ -1,4 +1,5 @@
-// Device building blocks of the B200 partition solver.
+// Device building blocks of the B200 partition solver (T = double or float,
+// as the reference's TridiagonalSystem<Real> / solve_partition<Real>).
 //
 // Terminology (reference: /root/reference/proj/include/tridpart/partition.hpp):
 //   * A "segment" is a run of consecutive rows [s, e] of one level's system.
@@ -25,23 +26,25 @@
 
 namespace tpb {
 
-// kPivotFloor<double> — tridiagonal.hpp:15-16
-constexpr double kPivotFloor = 1e-30;
+// kPivotFloor<Real> = Real(1e-30) — tridiagonal.hpp:15-16
+template <class T>
+__device__ __forceinline__ T pivot_floor() { return T(1e-30); }
 
-
+template <class T>
 struct Eq2 {
-    double a1, b1, g1, d1;  // E1
-    double a2, b2, g2, d2;  // E2
+    T a1, b1, g1, d1;  // E1
+    T a2, b2, g2, d2;  // E2
 };
 
 // Saved per merge for the top-down pass: x_t = (d1 - a2*x_s - g1*x_e) * r1
+template <class T>
 struct MergeSave {
-    double d1, g1, r1, a2;
+    T d1, g1, r1, a2;
 };
 
-// FP64 reciprocal: MUFU.RCP64H seed + one cubic Newton step, <= 1 ulp from the
-// correctly rounded 1/x (checked on the GPU by tp_diag_rcp_ulp); no slow path,
-// because every pivot it sees passed the |p| >= 1e-30 floor check (or is
+// Reciprocals: MUFU seed + one Newton-type step, <= 1 ulp from the correctly
+// rounded 1/x (FP64 checked on the GPU by tp_diag_rcp_ulp); no slow path,
+// because every pivot they see passed the |p| >= 1e-30 floor check (or is
 // already reported as a zero pivot). w = c * rcp(p) replaces the reference's
 // c / p (<= ~2 ulp apart; parity is by tolerance).
 __device__ __forceinline__ double rcp(double x) {
@@ -51,21 +54,28 @@ __device__ __forceinline__ double rcp(double x) {
     const double e = fma(-x, r, 1.0);
     return fma(r, fma(e, e, e), r);
 }
+__device__ __forceinline__ float rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
 
 // Zero-pivot bookkeeping (|pivot| < kPivotFloor -> ZeroPivotError).
 // RowGuard remembers the smallest offending row (generic / finishing paths);
-// MinGuard keeps only min|pivot| (one DMNMX per pivot on the hot path) and the
+// MinGuard keeps only min|pivot| (one min per pivot on the hot path) and the
 // caller reports the chunk's first row when it fell below the floor.
 struct RowGuard {
     int64_t bad = INT64_MAX;
-    __device__ __forceinline__ void see(double p, int64_t row) {
-        if (fabs(p) < kPivotFloor) bad = (row < bad) ? row : bad;
+    template <class T>
+    __device__ __forceinline__ void see(T p, int64_t row) {
+        if (fabs(p) < pivot_floor<T>()) bad = (row < bad) ? row : bad;
     }
 };
+template <class T>
 struct MinGuard {
-    double pmin = 1.0e300;
-    __device__ __forceinline__ void see(double p, int64_t) { pmin = fmin(pmin, fabs(p)); }
-    __device__ __forceinline__ bool tripped() const { return pmin < kPivotFloor; }
+    T pmin = T(1.0e30);
+    __device__ __forceinline__ void see(T p, int64_t) { pmin = fmin(pmin, fabs(p)); }
+    __device__ __forceinline__ bool tripped() const { return pmin < pivot_floor<T>(); }
 };
 
 // err word encodes (level << 48) | row; atomicMin keeps the lexicographically
@@ -84,17 +94,17 @@ __device__ __forceinline__ void report_pivot(unsigned long long* err, int level,
 // (K == L on the fixed-shape path; k_fast_rt dispatches on a runtime length).
 // up-sweep  = partition.hpp:90-108, down-sweep = partition.hpp:110-124.
 // ---------------------------------------------------------------------------
-template <int L>
+template <class T, int L>
 struct Chunk {
-    double a[L], b[L], c[L], d[L];
+    T a[L], b[L], c[L], d[L];
 };
 
 // Stage-1 leaf: E1/E2 only (no per-row storage).
-template <int L, int len, class G>
-__device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int64_t row0, G& bad) {
-    Eq2 q;
+template <class T, int L, int len, class Gd>
+__device__ __forceinline__ Eq2<T> leaf_reduce(const Chunk<T, L>& r, int64_t row0, Gd& bad) {
+    Eq2<T> q;
     // up-sweep: seed row len-2, run i = len-3 .. 0
-    double beta = 0, gamma = 0, delta = 0;
+    T beta = 0, gamma = 0, delta = 0;
 #pragma unroll
     for (int i = L - 2; i >= 0; --i) {
         if (i == len - 2) {
@@ -103,7 +113,7 @@ __device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int64_t row0, G& b
             delta = r.d[i];
         } else if (i < len - 2) {
             bad.see(beta, row0 + i + 1);
-            const double w = r.c[i] * rcp(beta);
+            const T w = r.c[i] * rcp(beta);
             beta = r.b[i] - w * r.a[i + 1];
             gamma = -w * gamma;
             delta = r.d[i] - w * delta;
@@ -114,13 +124,13 @@ __device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int64_t row0, G& b
     q.g1 = gamma;
     q.d1 = delta;
     // down-sweep: seed row 1, run i = 2 .. len-1
-    double phi = r.a[1], bp = r.b[1], dp = r.d[1];
-    double glast = r.c[1];
+    T phi = r.a[1], bp = r.b[1], dp = r.d[1];
+    T glast = r.c[1];
 #pragma unroll
     for (int i = 2; i < L; ++i) {
         if (i < len) {
             bad.see(bp, row0 + i - 1);
-            const double w = r.a[i] * rcp(bp);
+            const T w = r.a[i] * rcp(bp);
             phi = -w * phi;
             bp = r.b[i] - w * r.c[i - 1];
             dp = r.d[i] - w * dp;
@@ -136,12 +146,11 @@ __device__ __forceinline__ Eq2 leaf_reduce(const Chunk<L>& r, int64_t row0, G& b
 
 // Stage-3 leaf: same sweeps, but keeps rcp(beta_i), gamma_i, delta_i of the
 // interior rows for back_substitute (partition.hpp:156-172).
-template <int L, int len, class G>
-__device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int64_t row0,
-                                                G& bad, double (&rbeta)[L],
-                                                double (&gam)[L], double (&del)[L]) {
-    Eq2 q;
-    double beta = 0, gamma = 0, delta = 0;
+template <class T, int L, int len, class Gd>
+__device__ __forceinline__ Eq2<T> leaf_reduce_keep(const Chunk<T, L>& r, int64_t row0, Gd& bad,
+                                                   T (&rbeta)[L], T (&gam)[L], T (&del)[L]) {
+    Eq2<T> q;
+    T beta = 0, gamma = 0, delta = 0;
 #pragma unroll
     for (int i = L - 2; i >= 0; --i) {
         if (i == len - 2) {
@@ -150,9 +159,9 @@ __device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int64_t row0,
             delta = r.d[i];
         } else if (i < len - 2) {
             bad.see(beta, row0 + i + 1);
-            const double rb = rcp(beta);
+            const T rb = rcp(beta);
             rbeta[i + 1] = rb;
-            const double w = r.c[i] * rb;
+            const T w = r.c[i] * rb;
             beta = r.b[i] - w * r.a[i + 1];
             gamma = -w * gamma;
             delta = r.d[i] - w * delta;
@@ -164,13 +173,13 @@ __device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int64_t row0,
     q.b1 = beta;
     q.g1 = gamma;
     q.d1 = delta;
-    double phi = r.a[1], bp = r.b[1], dp = r.d[1];
-    double glast = r.c[1];
+    T phi = r.a[1], bp = r.b[1], dp = r.d[1];
+    T glast = r.c[1];
 #pragma unroll
     for (int i = 2; i < L; ++i) {
         if (i < len) {
             bad.see(bp, row0 + i - 1);
-            const double w = r.a[i] * rcp(bp);
+            const T w = r.a[i] * rcp(bp);
             phi = -w * phi;
             bp = r.b[i] - w * r.c[i - 1];
             dp = r.d[i] - w * dp;
@@ -185,16 +194,16 @@ __device__ __forceinline__ Eq2 leaf_reduce_keep(const Chunk<L>& r, int64_t row0,
 }
 
 // Interior of a chunk from its end values: back_substitute, partition.hpp:163-170.
-template <int L, int len>
-__device__ __forceinline__ void leaf_expand(const Chunk<L>& r, const double (&rbeta)[L],
-                                            const double (&gam)[L], const double (&del)[L],
-                                            double xs, double xe, double (&x)[L]) {
+template <class T, int L, int len>
+__device__ __forceinline__ void leaf_expand(const Chunk<T, L>& r, const T (&rbeta)[L],
+                                            const T (&gam)[L], const T (&del)[L], T xs, T xe,
+                                            T (&x)[L]) {
     x[0] = xs;
-    double prev = xs;
+    T prev = xs;
 #pragma unroll
     for (int i = 1; i < L; ++i) {
         if (i < len - 1) {
-            const double xi = (del[i] - r.a[i] * prev - gam[i] * xe) * rbeta[i];
+            const T xi = (del[i] - r.a[i] * prev - gam[i] * xe) * rbeta[i];
             x[i] = xi;
             prev = xi;
         } else if (i == len - 1) {
@@ -207,31 +216,31 @@ __device__ __forceinline__ void leaf_expand(const Chunk<L>& r, const double (&rb
 // Merge of adjacent segments A=[s,t], B=[t+1,e]: reduce_block on the 4-row
 // system [A.E1, A.E2, B.E1, B.E2] in the unknowns (x_s, x_t, x_{t+1}, x_e).
 // ---------------------------------------------------------------------------
-template <class G>
-__device__ __forceinline__ Eq2 merge(const Eq2& A, const Eq2& B, int64_t row_t, G& bad,
-                                     MergeSave& sv) {
-    Eq2 P;
+template <class T, class Gd>
+__device__ __forceinline__ Eq2<T> merge(const Eq2<T>& A, const Eq2<T>& B, int64_t row_t, Gd& bad,
+                                        MergeSave<T>& sv) {
+    Eq2<T> P;
     // up-sweep: seed row 2 (= B.E1), then row 1 (= A.E2), then row 0 (= A.E1)
     bad.see(B.b1, row_t + 1);
-    const double w1 = A.g2 * rcp(B.b1);
-    const double beta1 = A.b2 - w1 * B.a1;
-    const double gamma1 = -w1 * B.g1;
-    const double delta1 = A.d2 - w1 * B.d1;
+    const T w1 = A.g2 * rcp(B.b1);
+    const T beta1 = A.b2 - w1 * B.a1;
+    const T gamma1 = -w1 * B.g1;
+    const T delta1 = A.d2 - w1 * B.d1;
     bad.see(beta1, row_t);
-    const double r1 = rcp(beta1);
-    const double w0 = A.g1 * r1;
+    const T r1 = rcp(beta1);
+    const T w0 = A.g1 * r1;
     P.a1 = A.a1;
     P.b1 = A.b1 - w0 * A.a2;
     P.g1 = -w0 * gamma1;
     P.d1 = A.d1 - w0 * delta1;
     // down-sweep: seed row 1 (= A.E2), then rows 2, 3
     bad.see(A.b2, row_t);
-    const double w2 = B.a1 * rcp(A.b2);
-    const double phi = -w2 * A.a2;
-    const double bp = B.b1 - w2 * A.g2;
-    const double dp = B.d1 - w2 * A.d2;
+    const T w2 = B.a1 * rcp(A.b2);
+    const T phi = -w2 * A.a2;
+    const T bp = B.b1 - w2 * A.g2;
+    const T dp = B.d1 - w2 * A.d2;
     bad.see(bp, row_t + 1);
-    const double w3 = B.a2 * rcp(bp);
+    const T w3 = B.a2 * rcp(bp);
     P.a2 = -w3 * phi;
     P.b2 = B.b2 - w3 * B.g1;
     P.g2 = B.g2;
@@ -244,32 +253,34 @@ __device__ __forceinline__ Eq2 merge(const Eq2& A, const Eq2& B, int64_t row_t, 
 }
 
 // Top-down at a merge node: x_t from the saved up-sweep row (back_substitute).
-__device__ __forceinline__ double merge_xt(const MergeSave& sv, double xs, double xe) {
+template <class T>
+__device__ __forceinline__ T merge_xt(const MergeSave<T>& sv, T xs, T xe) {
     return (sv.d1 - sv.a2 * xs - sv.g1 * xe) * sv.r1;
 }
 // x_{t+1} = first row of B from its E1, given x_t and x_e.
-__device__ __forceinline__ double first_from_e1(const Eq2& B, double xt, double xe) {
+template <class T>
+__device__ __forceinline__ T first_from_e1(const Eq2<T>& B, T xt, T xe) {
     return (B.d1 - B.a1 * xt - B.g1 * xe) * rcp(B.b1);
 }
 
 // Solve the 2x2 root system of a whole (non-coupled) system by Thomas
 // (tridiagonal.hpp:52-72 on [E1; E2]); sub of row 0 / super of row 1 ignored,
 // exactly as thomas_solve never reads sub[0] and drops c'_{n-1}.
-template <class G>
-__device__ __forceinline__ void root_solve(const Eq2& q, int64_t row_last, G& bad,
-                                           double& x0, double& x1) {
+template <class T, class Gd>
+__device__ __forceinline__ void root_solve(const Eq2<T>& q, int64_t row_last, Gd& bad, T& x0, T& x1) {
     bad.see(q.b1, 0);
-    const double r0 = rcp(q.b1);
-    const double cm = q.g1 * r0;
-    const double xp = q.d1 * r0;
-    const double piv = q.b2 - q.a2 * cm;
+    const T r0 = rcp(q.b1);
+    const T cm = q.g1 * r0;
+    const T xp = q.d1 * r0;
+    const T piv = q.b2 - q.a2 * cm;
     bad.see(piv, row_last);
     x1 = (q.d2 - q.a2 * xp) * rcp(piv);
     x0 = xp - cm * x1;
 }
 
-__device__ __forceinline__ Eq2 shfl_down_eq(const Eq2& q, int delta) {
-    Eq2 r;
+template <class T>
+__device__ __forceinline__ Eq2<T> shfl_down_eq(const Eq2<T>& q, int delta) {
+    Eq2<T> r;
     r.a1 = __shfl_down_sync(0xffffffffu, q.a1, delta);
     r.b1 = __shfl_down_sync(0xffffffffu, q.b1, delta);
     r.g1 = __shfl_down_sync(0xffffffffu, q.g1, delta);
@@ -282,40 +293,78 @@ __device__ __forceinline__ Eq2 shfl_down_eq(const Eq2& q, int delta) {
 }
 
 // ---------------------------------------------------------------------------
-// Vectorised register loads/stores (256-bit LDG/STG on sm_100a).
+// Vectorised register loads/stores: 256-bit LDG/STG on sm_100a (4 doubles or
+// 8 floats per instruction).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void ld4(const double* p, double& x0, double& x1, double& x2,
-                                    double& x3) {
+__device__ __forceinline__ void ld256(const double* p, double* v) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3)
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
                  : "l"(p));
 }
-__device__ __forceinline__ void st4(double* p, double x0, double x1, double x2, double x3) {
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x0), "d"(x1), "d"(x2),
-                 "d"(x3)
+__device__ __forceinline__ void ld256(const float* p, float* v) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                   "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st256(double* p, const double* v) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]),
+                 "d"(v[3])
+                 : "memory");
+}
+__device__ __forceinline__ void st256(float* p, const float* v) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                  : "memory");
 }
 
-template <int L, bool VEC>
-__device__ __forceinline__ void load_rows(const double* __restrict__ p, int64_t r0, double (&v)[L]) {
-    if constexpr (VEC && (L % 4 == 0)) {
+// rows per 256-bit access
+template <class T>
+constexpr int vec_rows() { return 32 / (int)sizeof(T); }
+
+template <class T, int L, bool VEC>
+__device__ __forceinline__ void load_rows(const T* __restrict__ p, int64_t r0, T (&v)[L]) {
+    constexpr int W = vec_rows<T>();
+    if constexpr (VEC && (L % W == 0)) {
 #pragma unroll
-        for (int q = 0; q < L / 4; ++q) ld4(p + r0 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int q = 0; q < L / W; ++q) ld256(p + r0 + W * q, v + W * q);
     } else {
 #pragma unroll
         for (int i = 0; i < L; ++i) v[i] = __ldg(p + r0 + i);
     }
 }
 
-template <int L, bool VEC>
-__device__ __forceinline__ void store_rows(double* __restrict__ p, int64_t r0, const double (&v)[L]) {
-    if constexpr (VEC && (L % 4 == 0)) {
+template <class T, int L, bool VEC>
+__device__ __forceinline__ void store_rows(T* __restrict__ p, int64_t r0, const T (&v)[L]) {
+    constexpr int W = vec_rows<T>();
+    if constexpr (VEC && (L % W == 0)) {
 #pragma unroll
-        for (int q = 0; q < L / 4; ++q) st4(p + r0 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int q = 0; q < L / W; ++q) st256(p + r0 + W * q, v + W * q);
     } else {
 #pragma unroll
         for (int i = 0; i < L; ++i) p[r0 + i] = v[i];
     }
+}
+
+// Two consecutive values (an interface row pair / a block's ends) as one
+// vector access.
+__device__ __forceinline__ void store_pair(double* p, double x0, double x1) {
+    *reinterpret_cast<double2*>(p) = make_double2(x0, x1);
+}
+__device__ __forceinline__ void store_pair(float* p, float x0, float x1) {
+    *reinterpret_cast<float2*>(p) = make_float2(x0, x1);
+}
+template <class T>
+struct Pair {
+    T x, y;
+};
+__device__ __forceinline__ Pair<double> load_pair(const double* p) {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    return {v.x, v.y};
+}
+__device__ __forceinline__ Pair<float> load_pair(const float* p) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    return {v.x, v.y};
 }
 
 }  // namespace tpb

@@ -1,10 +1,11 @@
 // sm_100a kernels of the B200 partition solver (FP64, HBM-bound).
 //
 // Kernel map (reference call stack partition.hpp:191-224):
-//   k_fast<L,G,STAGE1>   parallel_for(reduce_block) + assemble_interface   :203-205
-//   k_fast<L,G,STAGE3>   parallel_for(back_substitute + scatter)            :214-222
-//   k_generic<MODE>      the same for any block length (tail blocks, odd m),
-//                        and the single-CTA finishing solve that replaces
+//   k_fast<T,L,G,STAGE1> parallel_for(reduce_block) + assemble_interface   :203-205
+//   k_fast<T,L,G,STAGE3> parallel_for(back_substitute + scatter)            :214-222
+//   k_fast_rt<T,...>     the same for any m <= 256 (runtime chunk lengths)
+//   k_generic<T,MODE>    the same for any block length (tail blocks, m > 256)
+//   k_final<T,MODE>      single-CTA finishing solve replacing
 //                        thomas_solve(iface) at the deepest level          :208-211
 //   k_gather_solve       sharded top level: Thomas on the all-gathered 2P rows
 //   k_generate           device-side counter-based generate_system analogue
@@ -24,31 +25,32 @@ namespace tpb {
 // a chunk of floor/ceil(blen/G) >= 2 rows. Lane-tree via shuffles below the
 // warp, via shared memory above it.
 // ===========================================================================
+template <class T>
 struct GenShared {
-    double* a;
-    double* b;
-    double* c;
-    double* d;
-    Eq2* xeq;       // one slot per warp (cross-warp merges)
-    double* xpass;  // 2 per warp (cross-warp top-down)
+    T* a;
+    T* b;
+    T* c;
+    T* d;
+    Eq2<T>* xeq;       // one slot per warp (cross-warp merges)
+    T* xpass;  // 2 per warp (cross-warp top-down)
 };
 
 // Leaf on a shared-memory chunk [p, p+len). When KEEP, overwrites b <- rcp(beta),
 // c <- gamma, d <- delta for the interior rows (consumed by leaf expansion).
-template <bool KEEP>
-__device__ Eq2 leaf_smem(double* a, double* b, double* c, double* d, int len, int64_t grow0,
+template <class T, bool KEEP>
+__device__ Eq2<T> leaf_smem(T* a, T* b, T* c, T* d, int len, int64_t grow0,
                          RowGuard& bad) {
-    Eq2 q;
+    Eq2<T> q;
     if (len == 1) {  // only in the n == 1 solve
         q.a1 = a[0]; q.b1 = b[0]; q.g1 = c[0]; q.d1 = d[0];
         q.a2 = a[0]; q.b2 = b[0]; q.g2 = c[0]; q.d2 = d[0];
         return q;
     }
     // down-sweep first (reads originals): partition.hpp:110-124
-    double phi = a[1], bp = b[1], dp = d[1];
+    T phi = a[1], bp = b[1], dp = d[1];
     for (int i = 2; i < len; ++i) {
         bad.see(bp, grow0 + i - 1);
-        const double w = a[i] * rcp(bp);
+        const T w = a[i] * rcp(bp);
         phi = -w * phi;
         bp = b[i] - w * c[i - 1];
         dp = d[i] - w * dp;
@@ -58,15 +60,15 @@ __device__ Eq2 leaf_smem(double* a, double* b, double* c, double* d, int len, in
     q.g2 = c[len - 1];
     q.d2 = dp;
     // up-sweep: partition.hpp:90-108
-    double beta = b[len - 2], gamma = c[len - 2], delta = d[len - 2];
+    T beta = b[len - 2], gamma = c[len - 2], delta = d[len - 2];
     if (KEEP) { c[len - 2] = gamma; d[len - 2] = delta; }
     for (int i = len - 3; i >= 0; --i) {
         bad.see(beta, grow0 + i + 1);
-        const double rb = rcp(beta);
-        const double w = c[i] * rb;
-        const double nb = b[i] - w * a[i + 1];
-        const double ng = -w * gamma;
-        const double nd = d[i] - w * delta;
+        const T rb = rcp(beta);
+        const T w = c[i] * rb;
+        const T nb = b[i] - w * a[i + 1];
+        const T ng = -w * gamma;
+        const T nd = d[i] - w * delta;
         if (KEEP) { b[i + 1] = rb; c[i] = ng; d[i] = nd; }
         beta = nb; gamma = ng; delta = nd;
     }
@@ -77,21 +79,22 @@ __device__ Eq2 leaf_smem(double* a, double* b, double* c, double* d, int len, in
     return q;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t row_base, int64_t blk_base, int64_t nblocks,
-                          int64_t blen, int G, IfacePtrs out, const double* __restrict__ xi,
-                          double* __restrict__ x, unsigned long long* err, int level) {
-    extern __shared__ __align__(16) double gsm[];
-    const int T = blockDim.x;
-    const int bpc = T / G;
+template <class T, int MODE>
+__global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs<T> sys, int64_t row_base, int64_t blk_base, int64_t nblocks,
+                          int64_t blen, int G, IfacePtrs<T> out, const T* __restrict__ xi,
+                          T* __restrict__ x, unsigned long long* err, int level) {
+    extern __shared__ __align__(16) unsigned char gsm_raw[];
+    T* gsm = reinterpret_cast<T*>(gsm_raw);
+    const int NT = blockDim.x;
+    const int bpc = NT / G;
     const int64_t tile_rows_max = (int64_t)bpc * blen;
-    GenShared s;
+    GenShared<T> s;
     s.a = gsm;
     s.b = s.a + tile_rows_max;
     s.c = s.b + tile_rows_max;
     s.d = s.c + tile_rows_max;
-    s.xeq = reinterpret_cast<Eq2*>(s.d + tile_rows_max);
-    s.xpass = reinterpret_cast<double*>(s.xeq + (T + 31) / 32);
+    s.xeq = reinterpret_cast<Eq2<T>*>(s.d + tile_rows_max);
+    s.xpass = reinterpret_cast<T*>(s.xeq + (NT + 31) / 32);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
         const int64_t nbt = (nblocks - b0) < bpc ? (nblocks - b0) : bpc;
         const int64_t trow0 = row_base + b0 * blen;
         const int64_t trows = nbt * blen;
-        for (int64_t i = tid; i < trows; i += T) {
+        for (int64_t i = tid; i < trows; i += NT) {
             s.a[i] = sys.sub[trow0 + i];
             s.b[i] = sys.diag[trow0 + i];
             s.c[i] = sys.sup[trow0 + i];
@@ -122,17 +125,17 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
         const bool active = lb < nbt;
         const int64_t lrow = (int64_t)lb * blen + off;  // local row of the chunk start
         const int64_t grow = trow0 + lrow;               // level row of the chunk start
-        Eq2 cur;
+        Eq2<T> cur;
         if (active) {
-            cur = leaf_smem<KEEP>(s.a + lrow, s.b + lrow, s.c + lrow, s.d + lrow, len, grow, bad);
+            cur = leaf_smem<T, KEEP>(s.a + lrow, s.b + lrow, s.c + lrow, s.d + lrow, len, grow, bad);
         } else {
-            cur = Eq2{0, 1, 0, 0, 0, 1, 0, 0};
+            cur = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
         }
         // ---- up the lane tree ----
-        MergeSave sv[10];
+        MergeSave<T> sv[10];
         for (int lv = 0; lv < logg; ++lv) {
             const int h = 1 << lv;
-            Eq2 oth;
+            Eq2<T> oth;
             if (h < 32) {
                 oth = shfl_down_eq(cur, h);
             } else {
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
             }
         }
         // ---- root ----
-        double xs = 0, xe = 0;
+        T xs = 0, xe = 0;
         if (c == 0 && active) {
             const int64_t jb = blk_base + b0 + lb;
             if (MODE == kStage1) {
@@ -174,9 +177,9 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
             // ---- down the lane tree ----
             for (int lv = logg - 1; lv >= 0; --lv) {
                 const int h = 1 << lv;
-                double xt = 0;
+                T xt = 0;
                 if ((c & (2 * h - 1)) == 0) xt = merge_xt(sv[lv], xs, xe);
-                double rxt, rxe;
+                T rxt, rxe;
                 if (h < 32) {
                     rxt = __shfl_up_sync(0xffffffffu, xt, h);
                     rxe = __shfl_up_sync(0xffffffffu, xe, h);
@@ -199,13 +202,13 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
             }
             // ---- leaf expansion into the a-slots, then coalesced store ----
             if (active) {
-                double* a = s.a + lrow;
-                const double* rb = s.b + lrow;
-                const double* g = s.c + lrow;
-                const double* dd = s.d + lrow;
-                double prev = xs;
+                T* a = s.a + lrow;
+                const T* rb = s.b + lrow;
+                const T* g = s.c + lrow;
+                const T* dd = s.d + lrow;
+                T prev = xs;
                 for (int i = 1; i < len - 1; ++i) {
-                    const double xv = (dd[i] - a[i] * prev - g[i] * xe) * rb[i];
+                    const T xv = (dd[i] - a[i] * prev - g[i] * xe) * rb[i];
                     a[i] = xv;
                     prev = xv;
                 }
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
                 if (len > 1) a[len - 1] = xe;
             }
             __syncthreads();
-            for (int64_t i = tid; i < trows; i += T) x[trow0 + i] = s.a[i];
+            for (int64_t i = tid; i < trows; i += NT) x[trow0 + i] = s.a[i];
         }
         __syncthreads();
         (void)lane;
@@ -234,18 +237,19 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs sys, int64_t 
 //        kStage1 (write the root E1/E2: the sharded reduce),
 //        kStage3 (root ends read from xi: the sharded expand).
 // ===========================================================================
-template <int MODE>
-__global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n, int G, IfacePtrs out,
-                                                         const double* __restrict__ xi,
-                                                         double* __restrict__ x,
+template <class T, int MODE>
+__global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_t n, int G, IfacePtrs<T> out,
+                                                         const T* __restrict__ xi,
+                                                         T* __restrict__ x,
                                                          unsigned long long* err, int level) {
-    extern __shared__ __align__(16) double fsm[];
-    double* sa = fsm;
-    double* sb = sa + n;
-    double* sc = sb + n;
-    double* sd = sc + n;
-    __shared__ Eq2 wroot[kFinalThreads2 / 32];
-    __shared__ double wx[2 * (kFinalThreads2 / 32)];
+    extern __shared__ __align__(16) unsigned char fsm_raw[];
+    T* fsm = reinterpret_cast<T*>(fsm_raw);
+    T* sa = fsm;
+    T* sb = sa + n;
+    T* sc = sb + n;
+    T* sd = sc + n;
+    __shared__ Eq2<T> wroot[kFinalThreads2 / 32];
+    __shared__ T wx[2 * (kFinalThreads2 / 32)];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     RowGuard bad;
 
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
     // paid once, not once per row
     {
         constexpr int kPer = (int)((kFinalCap + kFinalThreads2 - 1) / kFinalThreads2);
-        double va[kPer], vb[kPer], vc[kPer], vd[kPer];
+        T va[kPer], vb[kPer], vc[kPer], vd[kPer];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const int64_t i = tid + (int64_t)k * kFinalThreads2;
@@ -293,15 +297,15 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
     auto chunk_start = [&](int c) { return c * Llo + (c < ext ? c : ext); };
     constexpr bool KEEP = (MODE != kStage1);
 
-    Eq2 cur = Eq2{0, 1, 0, 0, 0, 1, 0, 0};
-    if (active) cur = leaf_smem<KEEP>(sa + off, sb + off, sc + off, sd + off, len, off, bad);
+    Eq2<T> cur = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
+    if (active) cur = leaf_smem<T, KEEP>(sa + off, sb + off, sc + off, sd + off, len, off, bad);
 
     // ---- warp-level tree (chunk index == tid) ----
-    MergeSave sw[5];
+    MergeSave<T> sw[5];
 #pragma unroll
     for (int lv = 0; lv < 5; ++lv) {
         const int h = 1 << lv;
-        const Eq2 oth = shfl_down_eq(cur, h);
+        const Eq2<T> oth = shfl_down_eq(cur, h);
         if (h < G && (lane & (2 * h - 1)) == 0 && tid + h < G)
             cur = merge(cur, oth, (int64_t)chunk_start(tid + h) - 1, bad, sw[lv]);
     }
@@ -311,16 +315,16 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
 
     // ---- warp 0: merge the warp roots, handle the root, push ends back down ----
     if (warp == 0) {
-        Eq2 wc = lane < nwr ? wroot[lane] : Eq2{0, 1, 0, 0, 0, 1, 0, 0};
-        MergeSave sx[5];
+        Eq2<T> wc = lane < nwr ? wroot[lane] : Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
+        MergeSave<T> sx[5];
 #pragma unroll
         for (int lv = 0; lv < 5; ++lv) {
             const int h = 1 << lv;
-            const Eq2 oth = shfl_down_eq(wc, h);
+            const Eq2<T> oth = shfl_down_eq(wc, h);
             if (h < nwr && (lane & (2 * h - 1)) == 0 && lane + h < nwr)
                 wc = merge(wc, oth, (int64_t)chunk_start(32 * (lane + h)) - 1, bad, sx[lv]);
         }
-        double xs = 0, xe = 0;
+        T xs = 0, xe = 0;
         if (lane == 0) {
             if (MODE == kStage1) {
                 out.sub[0] = wc.a1;  out.sub[1] = wc.a2;
@@ -339,10 +343,10 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
             for (int lv = 4; lv >= 0; --lv) {
                 const int h = 1 << lv;
                 if (h >= nwr) continue;
-                double xt = 0;
+                T xt = 0;
                 if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sx[lv], xs, xe);
-                const double rxt = __shfl_up_sync(0xffffffffu, xt, h);
-                const double rxe = __shfl_up_sync(0xffffffffu, xe, h);
+                const T rxt = __shfl_up_sync(0xffffffffu, xt, h);
+                const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
                 if ((lane & (2 * h - 1)) == h) {
                     xs = first_from_e1(wc, rxt, rxe);
                     xe = rxe;
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
     __syncthreads();
 
     // ---- every warp: its segment ends, then the warp-level tree top-down ----
-    double xs = 0, xe = 0;
+    T xs = 0, xe = 0;
     if (lane == 0 && warp < nwr) {
         xs = wx[2 * warp];
         xe = wx[2 * warp + 1];
@@ -372,10 +376,10 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
     for (int lv = 4; lv >= 0; --lv) {
         const int h = 1 << lv;
         if (h >= G) continue;
-        double xt = 0;
+        T xt = 0;
         if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sw[lv], xs, xe);
-        const double rxt = __shfl_up_sync(0xffffffffu, xt, h);
-        const double rxe = __shfl_up_sync(0xffffffffu, xe, h);
+        const T rxt = __shfl_up_sync(0xffffffffu, xt, h);
+        const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
         if ((lane & (2 * h - 1)) == h) {
             xs = first_from_e1(cur, rxt, rxe);
             xe = rxe;
@@ -385,13 +389,13 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
     }
     // ---- leaf back-substitution into the a-slots, then a coalesced store ----
     if (active) {
-        double* a = sa + off;
-        const double* rb = sb + off;
-        const double* g = sc + off;
-        const double* dd = sd + off;
-        double prev = xs;
+        T* a = sa + off;
+        const T* rb = sb + off;
+        const T* g = sc + off;
+        const T* dd = sd + off;
+        T prev = xs;
         for (int i = 1; i < len - 1; ++i) {
-            const double xv = (dd[i] - a[i] * prev - g[i] * xe) * rb[i];
+            const T xv = (dd[i] - a[i] * prev - g[i] * xe) * rb[i];
             a[i] = xv;
             prev = xv;
         }
@@ -403,52 +407,31 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs sys, int64_t n
     report_pivot(err, level, bad.bad);
 }
 
-size_t final_smem_bytes(int64_t n) { return (size_t)(4 * n) * sizeof(double); }
-
-int final_G(int64_t n) {
-    int G = 1;
-    while (G * 2 <= kFinalThreads2 && n / (G * 2) >= 2) G *= 2;
-    return G;
-}
-
-cudaError_t launch_final(int mode, const SysPtrs& sys, int64_t n, const IfacePtrs& out, const double* xi,
-                         double* x, unsigned long long* err, int level, cudaStream_t st) {
-    if (n > kFinalCap || n < 1) return cudaErrorInvalidValue;
-    const int G = final_G(n);
-    const size_t smem = final_smem_bytes(n);
-    if (mode == kStage1)
-        k_final<kStage1><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
-    else if (mode == kStage3)
-        k_final<kStage3><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
-    else
-        k_final<kSolve><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
-    return cudaGetLastError();
-}
-
 // ===========================================================================
 // Sharded top level: every rank holds the gathered [eq8 x P] (layout per rank:
 // sub[2], diag[2], sup[2], rhs[2]); assemble the 2P-row interface
 // (assemble_interface, partition.hpp:139-149) and solve it with Thomas
 // (tridiagonal.hpp:52-72) in one thread; keep this rank's (x_s, x_e).
 // ===========================================================================
-__global__ void k_gather_solve(const double* __restrict__ eqs, int nranks, int rank,
-                               double* __restrict__ x2, double* __restrict__ scratch,
+template <class T>
+__global__ void k_gather_solve(const T* __restrict__ eqs, int nranks, int rank,
+                               T* __restrict__ x2, T* __restrict__ scratch,
                                unsigned long long* err, int level) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int n = 2 * nranks;
-    double* cm = scratch;
-    double* xx = scratch + n;
+    T* cm = scratch;
+    T* xx = scratch + n;
     RowGuard bad;
     for (int i = 0; i < n; ++i) {
-        const double* e = eqs + 8 * (i >> 1);
+        const T* e = eqs + 8 * (i >> 1);
         const int k = i & 1;
-        const double sub = e[0 + k], dg = e[2 + k], sp = e[4 + k], rh = e[6 + k];
+        const T sub = e[0 + k], dg = e[2 + k], sp = e[4 + k], rh = e[6 + k];
         if (i == 0) {
             bad.see(dg, 0);
             cm[0] = sp / dg;
             xx[0] = rh / dg;
         } else {
-            const double piv = dg - sub * cm[i - 1];
+            const T piv = dg - sub * cm[i - 1];
             bad.see(piv, i);
             cm[i] = sp / piv;
             xx[i] = (rh - sub * xx[i - 1]) / piv;
@@ -467,6 +450,14 @@ __global__ void k_gather_solve(const double* __restrict__ eqs, int nranks, int r
 // so any shard generates its slice of the same global system. NOT
 // bit-identical to std::mt19937_64; used for throughput runs only.
 // ===========================================================================
+// ===========================================================================
+// Device generator: same distributions as generate_system (bench.hpp:68-93)
+// — a,c,d ~ U[-1,1), b = delta*(|a|+|c|)+1, whole-row sign flip with p=0.5,
+// sub[0] = super[N-1] = 0 — from a counter-based hash of (seed, global row),
+// so any shard generates its slice of the same global system. NOT
+// bit-identical to std::mt19937_64; used for throughput runs only. Values
+// are drawn in FP64 and rounded to T.
+// ===========================================================================
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
@@ -474,9 +465,10 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 }
 __device__ __forceinline__ double canon(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
 
+template <class T>
 __global__ void k_generate(int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
-                           double* __restrict__ sub, double* __restrict__ diag,
-                           double* __restrict__ sup, double* __restrict__ rhs) {
+                           T* __restrict__ sub, T* __restrict__ diag, T* __restrict__ sup,
+                           T* __restrict__ rhs) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t g = (uint64_t)(row0 + i);
@@ -489,25 +481,26 @@ __global__ void k_generate(int64_t n, int64_t row0, int64_t n_global, uint64_t s
         if (row0 + i == n_global - 1) cc = 0.0;
         double b = delta * (fabs(a) + fabs(cc)) + 1.0;
         if (fl) { a = -a; b = -b; cc = -cc; d = -d; }
-        sub[i] = a;
-        diag[i] = b;
-        sup[i] = cc;
-        rhs[i] = d;
+        sub[i] = (T)a;
+        diag[i] = (T)b;
+        sup[i] = (T)cc;
+        rhs[i] = (T)d;
     }
 }
 
 // residual_inf (tridiagonal.hpp:74-87): out[0] = max|Ax-d|, out[1] = max(1, max|d|),
-// both as order-preserving uint64 bit patterns of non-negative doubles.
-__global__ void k_residual(SysPtrs sys, int64_t n, const double* __restrict__ x,
-                           unsigned long long* out) {
+// accumulated in FP64 and kept as order-preserving uint64 bit patterns of
+// non-negative doubles.
+template <class T>
+__global__ void k_residual(SysPtrs<T> sys, int64_t n, const T* __restrict__ x, unsigned long long* out) {
     double num = 0, den = 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double ax = sys.diag[i] * x[i];
-        if (i > 0) ax += sys.sub[i] * x[i - 1];
-        if (i + 1 < n) ax += sys.sup[i] * x[i + 1];
-        num = fmax(num, fabs(ax - sys.rhs[i]));
-        den = fmax(den, fabs(sys.rhs[i]));
+        double ax = (double)sys.diag[i] * x[i];
+        if (i > 0) ax += (double)sys.sub[i] * x[i - 1];
+        if (i + 1 < n) ax += (double)sys.sup[i] * x[i + 1];
+        num = fmax(num, fabs(ax - (double)sys.rhs[i]));
+        den = fmax(den, fabs((double)sys.rhs[i]));
     }
     for (int o = 16; o > 0; o >>= 1) {
         num = fmax(num, __shfl_down_sync(0xffffffffu, num, o));
@@ -522,88 +515,104 @@ __global__ void k_residual(SysPtrs sys, int64_t n, const double* __restrict__ x,
 // ===========================================================================
 // Launchers
 // ===========================================================================
+
 // Launch shapes chosen by measurement (scratch/tune.cu on B200, N=1e8, m=64):
 // Stage 1  128 threads, <=80 regs (6 CTAs/SM), one chunk per thread (full grid)
 // Stage 3  128 threads, <=128 regs (4 CTAs/SM), persistent grid-stride
-template <int L, int G, int MODE, bool VEC>
+template <class T, int L, int G, int MODE, bool VEC>
 struct FastCfg {
     static constexpr int kThreads = 128;
     static constexpr int kMinBlocks = (MODE == kStage1) ? 6 : 4;
-    static constexpr bool kPersistent = (MODE != kStage1);
-    static void* fn() { return (void*)k_fast<L, G, MODE, VEC, kThreads, kMinBlocks>; }
+    static void* fn() { return (void*)k_fast<T, L, G, MODE, VEC, kThreads, kMinBlocks>; }
 };
 
-template <int L, int G, bool VEC>
-static cudaError_t launch_fast_t(int mode, const SysPtrs& sys, int64_t nblocks, const IfacePtrs& out,
-                                 const double* xi, double* x, unsigned long long* err, int level,
-                                 int grid_cap, cudaStream_t st) {
+template <class T, int L, int G, bool VEC>
+static cudaError_t launch_fast_t(int mode, const SysPtrs<T>& sys, int64_t nblocks,
+                                 const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
+                                 int level, int grid_cap, cudaStream_t st) {
     const int64_t nchunks = nblocks * G;
     if (mode == kStage1) {
-        using C = FastCfg<L, G, kStage1, VEC>;
+        using C = FastCfg<T, L, G, kStage1, VEC>;
         int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
         if (grid < 1) grid = 1;
-        k_fast<L, G, kStage1, VEC, C::kThreads, C::kMinBlocks><<<(unsigned)grid, C::kThreads, 0, st>>>(
+        k_fast<T, L, G, kStage1, VEC, C::kThreads, C::kMinBlocks><<<(unsigned)grid, C::kThreads, 0, st>>>(
             sys, nblocks, out, xi, x, err, level);
     } else {
-        using C = FastCfg<L, G, kStage3, VEC>;
+        using C = FastCfg<T, L, G, kStage3, VEC>;
         int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
         if (grid > grid_cap) grid = grid_cap;
         if (grid < 1) grid = 1;
-        k_fast<L, G, kStage3, VEC, C::kThreads, C::kMinBlocks><<<(unsigned)grid, C::kThreads, 0, st>>>(
+        k_fast<T, L, G, kStage3, VEC, C::kThreads, C::kMinBlocks><<<(unsigned)grid, C::kThreads, 0, st>>>(
             sys, nblocks, out, xi, x, err, level);
     }
     return cudaGetLastError();
 }
 
-template <int L, int G>
-static cudaError_t launch_fast_v(bool vec, int mode, const SysPtrs& sys, int64_t nblocks,
-                                 const IfacePtrs& out, const double* xi, double* x,
-                                 unsigned long long* err, int level, int grid_cap, cudaStream_t st) {
-    if (vec) return launch_fast_t<L, G, true>(mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
-    return launch_fast_t<L, G, false>(mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
+template <class T, int L, int G>
+static cudaError_t launch_fast_v(bool vec, int mode, const SysPtrs<T>& sys, int64_t nblocks,
+                                 const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
+                                 int level, int grid_cap, cudaStream_t st) {
+    if (vec) return launch_fast_t<T, L, G, true>(mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
+    return launch_fast_t<T, L, G, false>(mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
 }
+
+// m -> (rows per lane L, lanes per block G) of the fixed-shape kernels
+#define TPB_FAST_SHAPES(X) \
+    X(4, 4, 1)             \
+    X(5, 5, 1)             \
+    X(8, 8, 1)             \
+    X(10, 5, 2)            \
+    X(16, 8, 2)            \
+    X(20, 5, 4)            \
+    X(32, 8, 4)            \
+    X(40, 5, 8)            \
+    X(64, 8, 8)            \
+    X(80, 5, 16)           \
+    X(128, 8, 16)          \
+    X(160, 5, 32)          \
+    X(256, 8, 32)
 
 bool fast_shape(int64_t m, int* L, int* G) {
+#define TPB_SHAPE(MM, LL, GG) \
+    case MM: *L = LL; *G = GG; return true;
     switch (m) {
-        case 4: *L = 4; *G = 1; return true;
-        case 5: *L = 5; *G = 1; return true;
-        case 8: *L = 8; *G = 1; return true;
-        case 10: *L = 5; *G = 2; return true;
-        case 16: *L = 8; *G = 2; return true;
-        case 20: *L = 5; *G = 4; return true;
-        case 32: *L = 8; *G = 4; return true;
-        case 40: *L = 5; *G = 8; return true;
-        case 64: *L = 8; *G = 8; return true;
-        case 80: *L = 5; *G = 16; return true;
-        case 128: *L = 8; *G = 16; return true;
-        case 160: *L = 5; *G = 32; return true;
-        case 256: *L = 8; *G = 32; return true;
+        TPB_FAST_SHAPES(TPB_SHAPE)
         default: return false;
     }
+#undef TPB_SHAPE
 }
 
-cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs& sys, int64_t nblocks,
-                        const IfacePtrs& out, const double* xi, double* x, unsigned long long* err,
+template <class T>
+cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs<T>& sys, int64_t nblocks,
+                        const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
                         int level, int grid_cap, cudaStream_t st) {
 #define TPB_CASE(MM, LL, GG) \
-    case MM: return launch_fast_v<LL, GG>(vec, mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
+    case MM: return launch_fast_v<T, LL, GG>(vec, mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
     switch (m) {
-        TPB_CASE(4, 4, 1)
-        TPB_CASE(5, 5, 1)
-        TPB_CASE(8, 8, 1)
-        TPB_CASE(10, 5, 2)
-        TPB_CASE(16, 8, 2)
-        TPB_CASE(20, 5, 4)
-        TPB_CASE(32, 8, 4)
-        TPB_CASE(40, 5, 8)
-        TPB_CASE(64, 8, 8)
-        TPB_CASE(80, 5, 16)
-        TPB_CASE(128, 8, 16)
-        TPB_CASE(160, 5, 32)
-        TPB_CASE(256, 8, 32)
+        TPB_FAST_SHAPES(TPB_CASE)
         default: return cudaErrorInvalidValue;
     }
 #undef TPB_CASE
+}
+
+template <class T>
+int fast_max_active_blocks(int64_t m, bool vec, int mode) {
+    int nb = 0;
+#define TPB_OCC(MM, LL, GG)                                                                         \
+    case MM: {                                                                                      \
+        void* fn = mode == kStage1 ? (vec ? FastCfg<T, LL, GG, kStage1, true>::fn()                  \
+                                          : FastCfg<T, LL, GG, kStage1, false>::fn())                \
+                                   : (vec ? FastCfg<T, LL, GG, kStage3, true>::fn()                  \
+                                          : FastCfg<T, LL, GG, kStage3, false>::fn());               \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0);                             \
+        break;                                                                                      \
+    }
+    switch (m) {
+        TPB_FAST_SHAPES(TPB_OCC)
+        default: break;
+    }
+#undef TPB_OCC
+    return nb;
 }
 
 // Runtime-length register path (k_fast_rt): the G with ceil(m/G) <= 8, m/G >= 2.
@@ -614,21 +623,22 @@ int fast_rt_G(int64_t m) {
     return (G <= 32 && m / G >= 2) ? G : 0;
 }
 
-cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs& sys, int64_t nblocks, const IfacePtrs& out,
-                           const double* xi, double* x, unsigned long long* err, int level, int sms,
-                           cudaStream_t st) {
+template <class T>
+cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs<T>& sys, int64_t nblocks,
+                           const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
+                           int level, int sms, cudaStream_t st) {
     const int G = fast_rt_G(m);
     if (G == 0) return cudaErrorInvalidValue;
     const int64_t nchunks = nblocks * G;
     int64_t grid = (nchunks + 127) / 128;
     if (mode != kStage1 && grid > (int64_t)sms * 4) grid = (int64_t)sms * 4;
     if (grid < 1) grid = 1;
-#define TPB_RT(GG)                                                                                   \
-    case GG:                                                                                         \
-        if (mode == kStage1)                                                                         \
-            k_fast_rt<8, GG, kStage1><<<(unsigned)grid, 128, 0, st>>>(sys, nblocks, m, out, xi, x, err, level); \
-        else                                                                                         \
-            k_fast_rt<8, GG, kStage3><<<(unsigned)grid, 128, 0, st>>>(sys, nblocks, m, out, xi, x, err, level); \
+#define TPB_RT(GG)                                                                                     \
+    case GG:                                                                                           \
+        if (mode == kStage1)                                                                           \
+            k_fast_rt<T, 8, GG, kStage1><<<(unsigned)grid, 128, 0, st>>>(sys, nblocks, m, out, xi, x, err, level); \
+        else                                                                                           \
+            k_fast_rt<T, 8, GG, kStage3><<<(unsigned)grid, 128, 0, st>>>(sys, nblocks, m, out, xi, x, err, level); \
         break;
     switch (G) {
         TPB_RT(1)
@@ -643,96 +653,118 @@ cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs& sys, int64_t nblo
     return cudaGetLastError();
 }
 
-size_t generic_smem_bytes(int threads, int G, int64_t blen) {
+size_t generic_smem_bytes(int threads, int G, int64_t blen, size_t elem) {
     const int64_t bpc = threads / G;
-    return (size_t)(4 * bpc * blen) * sizeof(double) + (size_t)((threads + 31) / 32) * sizeof(Eq2) +
-           (size_t)(2 * ((threads + 31) / 32)) * sizeof(double);
+    const size_t warps = (size_t)((threads + 31) / 32);
+    return (size_t)(4 * bpc * blen) * elem + warps * 8 * elem + warps * 2 * elem;
 }
 
-cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs& sys, int64_t row_base,
-                           int64_t blk_base, int64_t nblocks, int64_t blen, const IfacePtrs& out,
-                           const double* xi, double* x, unsigned long long* err, int level,
-                           cudaStream_t st) {
-    const size_t smem = generic_smem_bytes(threads, G, blen);
+template <class T>
+cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs<T>& sys,
+                           int64_t row_base, int64_t blk_base, int64_t nblocks, int64_t blen,
+                           const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
+                           int level, cudaStream_t st) {
+    const size_t smem = generic_smem_bytes(threads, G, blen, sizeof(T));
     if (smem > kMaxDynSmem) return cudaErrorInvalidValue;
     if (mode == kStage1) {
-        k_generic<kStage1><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
+        k_generic<T, kStage1><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
     } else if (mode == kStage3) {
-        k_generic<kStage3><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
+        k_generic<T, kStage3><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
     } else {
-        k_generic<kSolve><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
+        k_generic<T, kSolve><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
     }
     return cudaGetLastError();
 }
 
-cudaError_t init_kernel_attributes() {
-    cudaError_t e = cudaFuncSetAttribute(k_generic<kStage1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_generic<kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_generic<kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+static int final_G(int64_t n) {
+    int G = 1;
+    while (G * 2 <= kFinalThreads2 && n / (G * 2) >= 2) G *= 2;
+    return G;
+}
+
+template <class T>
+cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const IfacePtrs<T>& out,
+                         const T* xi, T* x, unsigned long long* err, int level, cudaStream_t st) {
+    if (n > kFinalCap || n < 1) return cudaErrorInvalidValue;
+    const int G = final_G(n);
+    const size_t smem = (size_t)(4 * n) * sizeof(T);
+    if (mode == kStage1)
+        k_final<T, kStage1><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
+    else if (mode == kStage3)
+        k_final<T, kStage3><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
+    else
+        k_final<T, kSolve><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
+    return cudaGetLastError();
+}
+
+template <class T>
+static cudaError_t set_smem_attributes() {
     const int fs = (int)(kMaxDynSmem - 4096);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<kStage1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+    cudaError_t e = cudaFuncSetAttribute(k_generic<T, kStage1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_generic<T, kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_generic<T, kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kStage1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
     return e;
 }
 
-cudaError_t launch_gather_solve(const double* eqs, int nranks, int rank, double* x2, double* scratch,
+cudaError_t init_kernel_attributes() {
+    cudaError_t e = set_smem_attributes<double>();
+    if (e == cudaSuccess) e = set_smem_attributes<float>();
+    return e;
+}
+
+template <class T>
+cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st) {
-    k_gather_solve<<<1, 32, 0, st>>>(eqs, nranks, rank, x2, scratch, err, level);
+    k_gather_solve<T><<<1, 32, 0, st>>>(eqs, nranks, rank, x2, scratch, err, level);
     return cudaGetLastError();
 }
 
+template <class T>
 cudaError_t launch_generate(int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
-                            double* sub, double* diag, double* sup, double* rhs, int sms,
-                            cudaStream_t st) {
+                            T* sub, T* diag, T* sup, T* rhs, int sms, cudaStream_t st) {
     int64_t grid = (n + 255) / 256;
     if (grid > (int64_t)sms * 16) grid = (int64_t)sms * 16;
     if (grid < 1) grid = 1;
-    k_generate<<<(unsigned)grid, 256, 0, st>>>(n, row0, n_global, seed, delta, sub, diag, sup, rhs);
+    k_generate<T><<<(unsigned)grid, 256, 0, st>>>(n, row0, n_global, seed, delta, sub, diag, sup, rhs);
     return cudaGetLastError();
 }
 
-cudaError_t launch_residual(const SysPtrs& sys, int64_t n, const double* x, unsigned long long* out,
+template <class T>
+cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsigned long long* out,
                             int sms, cudaStream_t st) {
     int64_t grid = (n + 255) / 256;
     if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
     if (grid < 1) grid = 1;
-    k_residual<<<(unsigned)grid, 256, 0, st>>>(sys, n, x, out);
+    k_residual<T><<<(unsigned)grid, 256, 0, st>>>(sys, n, x, out);
     return cudaGetLastError();
 }
 
-int fast_max_active_blocks(int64_t m, bool vec, int mode) {
-    int L, G, nb = 0;
-    if (!fast_shape(m, &L, &G)) return 0;
-#define TPB_OCC(MM, LL, GG)                                                                          \
-    case MM:                                                                                         \
-        if (mode == kStage1) {                                                                       \
-            if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, FastCfg<LL, GG, kStage1, true>::fn(), 128, 0); \
-            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, FastCfg<LL, GG, kStage1, false>::fn(), 128, 0); \
-        } else {                                                                                     \
-            if (vec) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, FastCfg<LL, GG, kStage3, true>::fn(), 128, 0); \
-            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, FastCfg<LL, GG, kStage3, false>::fn(), 128, 0); \
-        }                                                                                            \
-        break;
-    switch (m) {
-        TPB_OCC(4, 4, 1)
-        TPB_OCC(5, 5, 1)
-        TPB_OCC(8, 8, 1)
-        TPB_OCC(10, 5, 2)
-        TPB_OCC(16, 8, 2)
-        TPB_OCC(20, 5, 4)
-        TPB_OCC(32, 8, 4)
-        TPB_OCC(40, 5, 8)
-        TPB_OCC(64, 8, 8)
-        TPB_OCC(80, 5, 16)
-        TPB_OCC(128, 8, 16)
-        TPB_OCC(160, 5, 32)
-        TPB_OCC(256, 8, 32)
-        default: break;
-    }
-#undef TPB_OCC
-    return nb;
-}
+// explicit instantiations for the two element types of the C-ABI
+#define TPB_INSTANTIATE(T)                                                                          \
+    template int fast_max_active_blocks<T>(int64_t, bool, int);                                     \
+    template cudaError_t launch_fast<T>(int64_t, bool, int, const SysPtrs<T>&, int64_t,             \
+                                        const IfacePtrs<T>&, const T*, T*, unsigned long long*, int, \
+                                        int, cudaStream_t);                                         \
+    template cudaError_t launch_fast_rt<T>(int64_t, int, const SysPtrs<T>&, int64_t,                \
+                                           const IfacePtrs<T>&, const T*, T*, unsigned long long*,  \
+                                           int, int, cudaStream_t);                                 \
+    template cudaError_t launch_generic<T>(int, int, int, int, const SysPtrs<T>&, int64_t, int64_t, \
+                                           int64_t, int64_t, const IfacePtrs<T>&, const T*, T*,    \
+                                           unsigned long long*, int, cudaStream_t);                 \
+    template cudaError_t launch_final<T>(int, const SysPtrs<T>&, int64_t, const IfacePtrs<T>&,      \
+                                         const T*, T*, unsigned long long*, int, cudaStream_t);     \
+    template cudaError_t launch_gather_solve<T>(const T*, int, int, T*, T*, unsigned long long*,    \
+                                                int, cudaStream_t);                                 \
+    template cudaError_t launch_generate<T>(int64_t, int64_t, int64_t, uint64_t, double, T*, T*,    \
+                                            T*, T*, int, cudaStream_t);                             \
+    template cudaError_t launch_residual<T>(const SysPtrs<T>&, int64_t, const T*,                   \
+                                            unsigned long long*, int, cudaStream_t);
+TPB_INSTANTIATE(double)
+TPB_INSTANTIATE(float)
+#undef TPB_INSTANTIATE
 
 }  // namespace tpb
 

@@ -1,4 +1,6 @@
 // Internal launcher interface between the C-ABI layer and the sm_100a kernels.
+// Every launcher is a template over the element type T (double or float) and
+// is explicitly instantiated for both in tp_kernels.cu.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -15,47 +17,57 @@ constexpr int kGenericThreads = 256;
 constexpr int kFinalThreads = 1024;   // k_generic CTA cap
 constexpr int kFinalThreads2 = 512;   // k_final CTA
 // Largest system the single-CTA finishing solve keeps in shared memory
-// (32 B per row; 6144 rows = 192 KiB of the 227 KiB opt-in limit).
+// (32 B per FP64 row; 6144 rows = 192 KiB of the 227 KiB opt-in limit).
 constexpr int64_t kFinalCap = 6144;
 constexpr size_t kMaxDynSmem = 227 * 1024;
 constexpr unsigned long long kNoError = ~0ULL;
 
+template <class T>
 struct SysPtrs {
-    const double* sub;
-    const double* diag;
-    const double* sup;
-    const double* rhs;
+    const T* sub;
+    const T* diag;
+    const T* sup;
+    const T* rhs;
 };
+template <class T>
 struct IfacePtrs {
-    double* sub;
-    double* diag;
-    double* sup;
-    double* rhs;
+    T* sub;
+    T* diag;
+    T* sup;
+    T* rhs;
 };
 
 cudaError_t init_kernel_attributes();
 bool fast_shape(int64_t m, int* L, int* G);
-int fast_max_active_blocks(int64_t m, bool vec, int mode);
-cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs& sys, int64_t nblocks,
-                        const IfacePtrs& out, const double* xi, double* x, unsigned long long* err,
-                        int level, int grid_cap, cudaStream_t st);
 int fast_rt_G(int64_t m);
-cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs& sys, int64_t nblocks, const IfacePtrs& out,
-                           const double* xi, double* x, unsigned long long* err, int level, int sms,
-                           cudaStream_t st);
-size_t generic_smem_bytes(int threads, int G, int64_t blen);
-cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs& sys, int64_t row_base,
-                           int64_t blk_base, int64_t nblocks, int64_t blen, const IfacePtrs& out,
-                           const double* xi, double* x, unsigned long long* err, int level,
-                           cudaStream_t st);
-cudaError_t launch_final(int mode, const SysPtrs& sys, int64_t n, const IfacePtrs& out, const double* xi,
-                         double* x, unsigned long long* err, int level, cudaStream_t st);
-cudaError_t launch_gather_solve(const double* eqs, int nranks, int rank, double* x2, double* scratch,
+
+template <class T>
+int fast_max_active_blocks(int64_t m, bool vec, int mode);
+template <class T>
+cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs<T>& sys, int64_t nblocks,
+                        const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
+                        int level, int grid_cap, cudaStream_t st);
+template <class T>
+cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs<T>& sys, int64_t nblocks,
+                           const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
+                           int level, int sms, cudaStream_t st);
+size_t generic_smem_bytes(int threads, int G, int64_t blen, size_t elem);
+template <class T>
+cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs<T>& sys,
+                           int64_t row_base, int64_t blk_base, int64_t nblocks, int64_t blen,
+                           const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
+                           int level, cudaStream_t st);
+template <class T>
+cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const IfacePtrs<T>& out,
+                         const T* xi, T* x, unsigned long long* err, int level, cudaStream_t st);
+template <class T>
+cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st);
+template <class T>
 cudaError_t launch_generate(int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
-                            double* sub, double* diag, double* sup, double* rhs, int sms,
-                            cudaStream_t st);
-cudaError_t launch_residual(const SysPtrs& sys, int64_t n, const double* x, unsigned long long* out,
+                            T* sub, T* diag, T* sup, T* rhs, int sms, cudaStream_t st);
+template <class T>
+cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsigned long long* out,
                             int sms, cudaStream_t st);
 
 }  // namespace tpb

@@ -187,8 +187,12 @@ tp_status tp_default_model(int32_t which, int64_t* pairs_n, int32_t* pairs_label
         src_n = tpb_models::kDepthN;
         src_l = tpb_models::kDepthLabel;
         cnt = tpb_models::kDepthCount;
+    } else if (which == 2) {
+        src_n = tpb_models::kSize32N;
+        src_l = tpb_models::kSize32Label;
+        cnt = tpb_models::kSize32Count;
     } else {
-        set_err(err, TP_ERR_INVALID_ARGUMENT, "which must be 0 (size) or 1 (depth)");
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "which must be 0 (fp64 size), 1 (depth) or 2 (fp32 size)");
         return TP_ERR_INVALID_ARGUMENT;
     }
     if (npairs) *npairs = cnt;

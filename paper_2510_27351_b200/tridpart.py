@@ -187,16 +187,27 @@ def _is_torch(a) -> bool:
 
 class TridiagonalSystem:
     """SoA system (tridiagonal.hpp:22-46): row i reads
-    sub[i]*x[i-1] + diag[i]*x[i] + super[i]*x[i+1] = rhs[i]."""
+    sub[i]*x[i-1] + diag[i]*x[i] + super[i]*x[i+1] = rhs[i].
 
-    def __init__(self, sub, diag, super, rhs):  # noqa: A002 - reference field name
+    Element type as TridiagonalSystem<Real>: float64 by default, float32 when
+    ``dtype`` is float32 or the arrays already are float32."""
+
+    def __init__(self, sub, diag, super, rhs, dtype=None):  # noqa: A002 - reference field name
         if _is_torch(diag):
             self.sub, self.diag, self.super, self.rhs = sub, diag, super, rhs
         else:
-            self.sub = np.ascontiguousarray(sub, dtype=np.float64)
-            self.diag = np.ascontiguousarray(diag, dtype=np.float64)
-            self.super = np.ascontiguousarray(super, dtype=np.float64)
-            self.rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+            if dtype is None:
+                dtype = np.float32 if getattr(diag, "dtype", None) == np.float32 else np.float64
+            self.sub = np.ascontiguousarray(sub, dtype=dtype)
+            self.diag = np.ascontiguousarray(diag, dtype=dtype)
+            self.super = np.ascontiguousarray(super, dtype=dtype)
+            self.rhs = np.ascontiguousarray(rhs, dtype=dtype)
+
+    @property
+    def is_f32(self) -> bool:
+        if _is_torch(self.diag):
+            return str(self.diag.dtype) == "torch.float32"
+        return self.diag.dtype == np.float32
 
     def size(self) -> int:
         return int(self.diag.shape[0])
@@ -223,9 +234,12 @@ class TridiagonalSystem:
         return [C.c_void_p(a.ctypes.data) for a in (self.sub, self.diag, self.super, self.rhs)]
 
     def _dev_ptrs(self):
+        want = str(self.diag.dtype)
         for a in (self.sub, self.diag, self.super, self.rhs):
-            if not (a.is_cuda and a.is_contiguous()) or str(a.dtype) != "torch.float64":
-                raise ValueError("device systems need contiguous float64 CUDA tensors")
+            if not (a.is_cuda and a.is_contiguous()) or str(a.dtype) != want or \
+                    want not in ("torch.float64", "torch.float32"):
+                raise ValueError("device systems need contiguous float64 (or float32) CUDA tensors "
+                                 "of one dtype")
         return [C.c_void_p(a.data_ptr()) for a in (self.sub, self.diag, self.super, self.rhs)]
 
 
@@ -233,7 +247,7 @@ Tridiagonal = TridiagonalSystem
 
 
 def generate_system(n: int, seed: int, delta: float = 1.5, device: bool = False,
-                    row0: int = 0, n_global: Optional[int] = None):
+                    row0: int = 0, n_global: Optional[int] = None, dtype: str = "float64"):
     """Synthetic strictly dominant system with the distributions of
     generate_system (bench.hpp:68-93), generated ON THE DEVICE from a
     counter-based hash (not bit-identical to std::mt19937_64). Returns device
@@ -242,9 +256,11 @@ def generate_system(n: int, seed: int, delta: float = 1.5, device: bool = False,
 
     n_global = n if n_global is None else n_global
     ctx = context()
-    arrs = [torch.empty(n, dtype=torch.float64, device=f"cuda:{ctx.device}") for _ in range(4)]
+    tdt = torch.float32 if dtype in ("float32", "f32", np.float32) else torch.float64
+    arrs = [torch.empty(n, dtype=tdt, device=f"cuda:{ctx.device}") for _ in range(4)]
     stream = torch_stream()
-    _call(lib.tp_generate_system_f64_dev, ctx.handle, n, row0, n_global, C.c_uint64(seed), delta,
+    fn = lib.tp_generate_system_f32_dev if tdt == torch.float32 else lib.tp_generate_system_f64_dev
+    _call(fn, ctx.handle, n, row0, n_global, C.c_uint64(seed), delta,
           *[C.c_void_p(a.data_ptr()) for a in arrs], C.c_void_p(stream))
     if device:
         return TridiagonalSystem(*arrs)
@@ -256,10 +272,11 @@ def residual_inf(sys: TridiagonalSystem, x) -> float:
     if sys.on_device:
         ctx = context()
         out = C.c_double()
-        _call(lib.tp_residual_inf_f64_dev, ctx.handle, *sys._dev_ptrs(), sys.size(),
+        fn = lib.tp_residual_inf_f32_dev if sys.is_f32 else lib.tp_residual_inf_f64_dev
+        _call(fn, ctx.handle, *sys._dev_ptrs(), sys.size(),
               C.c_void_p(x.data_ptr()), C.byref(out))
         return float(out.value)
-    x = np.asarray(x, dtype=np.float64)
+    x = np.asarray(x, dtype=sys.diag.dtype)
     ax = sys.diag * x
     ax[1:] += sys.sub[1:] * x[:-1]
     ax[:-1] += sys.super[:-1] * x[1:]
@@ -273,8 +290,9 @@ def thomas_solve(sys: TridiagonalSystem) -> np.ndarray:
     device finishing solver."""
     ctx = context()
     n = sys.size()
-    x = np.empty(n, dtype=np.float64)
-    _call(lib.tp_thomas_solve_f64, ctx.handle, *sys._host_ptrs(), n, C.c_void_p(x.ctypes.data))
+    x = np.empty(n, dtype=sys.diag.dtype)
+    fn = lib.tp_thomas_solve_f32 if sys.is_f32 else lib.tp_thomas_solve_f64
+    _call(fn, ctx.handle, *sys._host_ptrs(), n, C.c_void_p(x.ctypes.data))
     return x
 
 
@@ -347,10 +365,12 @@ def solve_partition(sys: TridiagonalSystem, policy,
         err = TpError()
         _raise(lib.tp_check_device_error(ctx.handle, C.byref(err)), err)
         return x
-    x = np.empty(max(n, 0), dtype=np.float64)
+    f32 = sys.is_f32
+    x = np.empty(max(n, 0), dtype=np.float32 if f32 else np.float64)
     if on_interface is None:
-        _call(lib.tp_solve_partition_f64, ctx.handle, *sys._host_ptrs(), n,
-              sz.ctypes.data_as(_I64), len(sz), C.c_void_p(x.ctypes.data))
+        fn = lib.tp_solve_partition_f32 if f32 else lib.tp_solve_partition_f64
+        _call(fn, ctx.handle, *sys._host_ptrs(), n, sz.ctypes.data_as(_I64), len(sz),
+              C.c_void_p(x.ctypes.data))
         return x
 
     def _cb(level, m, a, b, c, d, _u):
@@ -359,9 +379,10 @@ def solve_partition(sys: TridiagonalSystem, policy,
                                        np.ctypeslib.as_array(c, (m,)).copy(),
                                        np.ctypeslib.as_array(d, (m,)).copy()), int(level))
 
-    cb = _lib.INTERFACE_CB(_cb)
-    _call(lib.tp_solve_partition_observe_f64, ctx.handle, *sys._host_ptrs(), n,
-          sz.ctypes.data_as(_I64), len(sz), C.c_void_p(x.ctypes.data), cb, None)
+    cb = (_lib.INTERFACE_CB_F32 if f32 else _lib.INTERFACE_CB)(_cb)
+    fn = lib.tp_solve_partition_observe_f32 if f32 else lib.tp_solve_partition_observe_f64
+    _call(fn, ctx.handle, *sys._host_ptrs(), n, sz.ctypes.data_as(_I64), len(sz),
+          C.c_void_p(x.ctypes.data), cb, None)
     return x
 
 
@@ -373,9 +394,10 @@ def solve_partition_async(sys: TridiagonalSystem, policy, out=None):
     sz = _policy_array(policy)
     ctx = context()
     n = sys.size()
-    x = out if out is not None else torch.empty(n, dtype=torch.float64, device=sys.diag.device)
+    x = out if out is not None else torch.empty(n, dtype=sys.diag.dtype, device=sys.diag.device)
     stream = torch_stream()
-    _call(lib.tp_solve_partition_f64_dev, ctx.handle, *sys._dev_ptrs(), n, sz.ctypes.data_as(_I64),
+    fn = lib.tp_solve_partition_f32_dev if sys.is_f32 else lib.tp_solve_partition_f64_dev
+    _call(fn, ctx.handle, *sys._dev_ptrs(), n, sz.ctypes.data_as(_I64),
           len(sz), C.c_void_p(x.data_ptr()), C.c_void_p(stream))
     return x
 
@@ -542,6 +564,13 @@ def default_size_model() -> HeuristicModel:
     """fit_knn(Table I FP64 with corrected labels, k=1) — what the reference's
     tests fit (test_policy.cpp:14-17)."""
     return _bundled(0)
+
+
+def default_fp32_size_model() -> HeuristicModel:
+    """fit_knn(Table IV FP32 with corrected labels, k=1)."""
+    m = _bundled(2)
+    m.metadata = {"device": "rtx2080ti", "precision": "fp32"}
+    return m
 
 
 def default_depth_model() -> HeuristicModel:

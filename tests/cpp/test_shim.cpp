@@ -112,6 +112,22 @@ int main() {
         try { recursion_sizes(1000000, 5, sm); } catch (const DepthOutOfRangeError&) { threw = true; }
         check(threw, "depth 5 throws DepthOutOfRangeError");
     }
+    {   // fp32 mode (test_partition.cpp:206-223): residual <= 1e-4
+        TridiagonalSystem<float> s;
+        const std::size_t n = 256;
+        s.sub.resize(n); s.diag.resize(n); s.super.resize(n); s.rhs.resize(n);
+        uint64_t st = 8;
+        auto unit = [&] { st = st * 6364136223846793005ULL + 1442695040888963407ULL;
+                          return (float)((double)(st >> 11) * 0x1.0p-53 * 2.0 - 1.0); };
+        for (std::size_t i = 0; i < n; ++i) {
+            s.sub[i] = i == 0 ? 0.f : unit();
+            s.super[i] = i + 1 == n ? 0.f : unit();
+            s.diag[i] = 1.5f * (std::abs(s.sub[i]) + std::abs(s.super[i])) + 1.f;
+            s.rhs[i] = unit();
+        }
+        const auto x = solve_partition(s, RecursionPolicy{{8, 4}});
+        check(residual_inf(s, x) <= 1e-4f, "fp32 solve_partition residual <= 1e-4");
+    }
     std::printf("%s\n", failures ? "FAILED" : "all passed");
     return failures ? 1 : 0;
 }
