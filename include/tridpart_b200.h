@@ -85,6 +85,16 @@ tp_status tp_solve_partition_f64_dev(tp_ctx* ctx, const double* sub, const doubl
                                      tp_error* err);
 tp_status tp_check_device_error(tp_ctx* ctx, tp_error* err);
 
+/* Host pointers, asynchronous on `stream` (NULL = ctx stream): the H2D copies,
+ * the device solve and the D2H copy are enqueued and the call returns. Host
+ * buffers should be pinned. Solves on two contexts / two streams overlap one
+ * solve's D2H with the next one's H2D (full-duplex PCIe). After synchronising
+ * the stream, tp_check_device_error reports zero pivots. */
+tp_status tp_solve_partition_f64_async(tp_ctx* ctx, const double* sub, const double* diag,
+                                       const double* super, const double* rhs, int64_t n,
+                                       const int64_t* sizes, int32_t nsizes, double* x, void* stream,
+                                       tp_error* err);
+
 /* Observer overload solve_partition(sys, policy, on_interface) — partition.hpp:235-242,
  * hook at :206. Host pointers; after the solve, `cb` receives each level's
  * assembled interface system (host copies, valid during the call), level 0 first. */
@@ -106,6 +116,10 @@ tp_status tp_solve_partition_f32_dev(tp_ctx* ctx, const float* sub, const float*
                                      const float* super, const float* rhs, int64_t n,
                                      const int64_t* sizes, int32_t nsizes, float* x, void* stream,
                                      tp_error* err);
+tp_status tp_solve_partition_f32_async(tp_ctx* ctx, const float* sub, const float* diag,
+                                       const float* super, const float* rhs, int64_t n,
+                                       const int64_t* sizes, int32_t nsizes, float* x, void* stream,
+                                       tp_error* err);
 tp_status tp_solve_partition_observe_f32(tp_ctx* ctx, const float* sub, const float* diag,
                                          const float* super, const float* rhs, int64_t n,
                                          const int64_t* sizes, int32_t nsizes, float* x,

@@ -42,7 +42,8 @@ EXPORTS = [
     "tp_predict", "tp_fit_knn", "tp_recursion_sizes", "tp_default_model", "tp_obs_read",
     "tp_obs_get", "tp_obs_free", "tp_diag_rcp_ulp", "tp_solve_partition_f32",
     "tp_solve_partition_f32_dev", "tp_solve_partition_observe_f32", "tp_thomas_solve_f32",
-    "tp_residual_inf_f32_dev", "tp_generate_system_f32_dev",
+    "tp_residual_inf_f32_dev", "tp_generate_system_f32_dev", "tp_solve_partition_f64_async",
+    "tp_solve_partition_f32_async",
 ]
 
 
@@ -93,6 +94,10 @@ def _load():
         "tp_solve_partition_observe_f32": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32,
                                                      vp, INTERFACE_CB_F32, vp, E]),
         "tp_thomas_solve_f32": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, E]),
+        "tp_solve_partition_f64_async": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
+                                                   vp, E]),
+        "tp_solve_partition_f32_async": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
+                                                   vp, E]),
         "tp_residual_inf_f32_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, _D, E]),
         "tp_generate_system_f32_dev": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
                                                  C.c_double, vp, vp, vp, vp, vp, E]),

@@ -509,13 +509,17 @@ tp_status solve_dev(tp_ctx* ctx, const T* sub, const T* diag, const T* super, co
 
 // H2D of the four arrays into the context's staging buffers, `body(device
 // arrays)` on the context stream, D2H of x, synchronise, decode zero pivots.
+// With `async`, everything is enqueued on `st` and the call returns at once
+// (host buffers should be pinned); zero pivots then surface through
+// tp_check_device_error after the caller synchronises.
 template <class T, class Body>
 tp_status host_roundtrip(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs,
-                         int64_t n, T* x, Body&& body, tp_error* err) {
+                         int64_t n, T* x, Body&& body, tp_error* err, cudaStream_t stream = nullptr,
+                         bool async = false) {
     T* d[5];
     tp_status s = ensure_dsys<T>(ctx, n, d, err);
     if (s != TP_OK) return s;
-    const cudaStream_t st = ctx->stream;
+    const cudaStream_t st = stream ? stream : ctx->stream;
     const size_t bytes = (size_t)n * sizeof(T);
     TP_CUDA(cudaMemcpyAsync(d[0], sub, bytes, cudaMemcpyHostToDevice, st));
     TP_CUDA(cudaMemcpyAsync(d[1], diag, bytes, cudaMemcpyHostToDevice, st));
@@ -524,9 +528,31 @@ tp_status host_roundtrip(tp_ctx* ctx, const T* sub, const T* diag, const T* supe
     s = body(d, st);
     if (s != TP_OK) return s;
     TP_CUDA(cudaMemcpyAsync(x, d[4], bytes, cudaMemcpyDeviceToHost, st));
+    if (async) return TP_OK;
     TP_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     TP_CUDA(cudaStreamSynchronize(st));
     return decode_device_error(ctx, err);
+}
+
+// Host buffers, asynchronous on `stream`: H2D, the device solve and D2H are
+// enqueued and the call returns. Two contexts on two streams let the D2H of
+// one solve overlap the H2D of the next (PCIe is full duplex).
+template <class T>
+tp_status solve_host_async(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs,
+                           int64_t n, const int64_t* sizes, int32_t nsizes, T* x, void* stream,
+                           tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    tp_status s = validate(sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    if (s != TP_OK) return s;
+    TP_CUDA(cudaSetDevice(ctx->device));
+    const cudaStream_t st = pick_stream(ctx, stream);
+    return host_roundtrip<T>(ctx, sub, diag, super, rhs, n, x,
+                             [&](T** d, cudaStream_t s2) {
+                                 return solve_dev<T>(ctx, d[0], d[1], d[2], d[3], n, sizes, nsizes,
+                                                     d[4], s2, err);
+                             },
+                             err, st, true);
 }
 
 template <class T>
@@ -837,6 +863,18 @@ tp_status tp_solve_partition_f32(tp_ctx* ctx, const float* sub, const float* dia
                                  const float* super, const float* rhs, int64_t n,
                                  const int64_t* sizes, int32_t nsizes, float* x, tp_error* err) {
     return solve_host<float>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, err);
+}
+tp_status tp_solve_partition_f64_async(tp_ctx* ctx, const double* sub, const double* diag,
+                                       const double* super, const double* rhs, int64_t n,
+                                       const int64_t* sizes, int32_t nsizes, double* x, void* stream,
+                                       tp_error* err) {
+    return solve_host_async<double>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, stream, err);
+}
+tp_status tp_solve_partition_f32_async(tp_ctx* ctx, const float* sub, const float* diag,
+                                       const float* super, const float* rhs, int64_t n,
+                                       const int64_t* sizes, int32_t nsizes, float* x, void* stream,
+                                       tp_error* err) {
+    return solve_host_async<float>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, stream, err);
 }
 tp_status tp_solve_partition_observe_f64(tp_ctx* ctx, const double* sub, const double* diag,
                                          const double* super, const double* rhs, int64_t n,

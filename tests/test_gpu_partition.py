@@ -318,3 +318,33 @@ def test_config4_n1e9_against_the_reference_itself(tp, oracle_mod):
         assert out[k]["rel_inf_diff"] <= TOL_NORM
         assert out[k]["floored_rel"] <= TOL_FLOOR
         assert out[k]["residual"] <= TOL_RES
+
+
+def test_async_host_solves_on_two_contexts(tp, oracle_mod):
+    """tp_solve_partition_f64_async: pinned host buffers, two contexts on two
+    streams in flight at once (the pipelined e2e path of bench.py)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_27351_b200._lib import lib
+    from paper_2510_27351_b200.tridpart import _call
+
+    n, sizes = 1_000_003, [32, 10, 16]
+    systems = [oracle_mod.generate_system(n, seed) for seed in (1, 2, 3, 4)]
+    refs = [oracle_mod.solve_partition(s, sizes) for s in systems]
+    pinned = [[torch.from_numpy(a).pin_memory() for a in (s.sub, s.diag, s.sup, s.rhs)] for s in systems]
+    outs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in systems]
+    ctxs = [tp.Context(torch.cuda.current_device()) for _ in range(2)]
+    strs = [torch.cuda.Stream() for _ in range(2)]
+    sz = np.asarray(sizes, dtype=np.int64)
+    for i, (arrs, out) in enumerate(zip(pinned, outs)):
+        _call(lib.tp_solve_partition_f64_async, ctxs[i % 2].handle,
+              *[C.c_void_p(a.data_ptr()) for a in arrs], n, sz.ctypes.data_as(C.POINTER(C.c_int64)),
+              len(sz), C.c_void_p(out.data_ptr()), C.c_void_p(strs[i % 2].cuda_stream))
+    for s_ in strs:
+        s_.synchronize()
+    for s, ref, out in zip(systems, refs, outs):
+        _check(oracle_mod, s, out.numpy(), ref)
+    for c in ctxs:
+        c.close()
