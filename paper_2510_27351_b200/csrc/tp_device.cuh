@@ -320,7 +320,7 @@ __device__ __forceinline__ void st256(float* p, const float* v) {
 
 // rows per 256-bit access
 template <class T>
-constexpr int vec_rows() { return 32 / (int)sizeof(T); }
+__host__ __device__ constexpr int vec_rows() { return 32 / (int)sizeof(T); }
 
 template <class T, int L, bool VEC>
 __device__ __forceinline__ void load_rows(const T* __restrict__ p, int64_t r0, T (&v)[L]) {

@@ -255,7 +255,11 @@ def main(argv=None):
     ap.add_argument("--out", default="sweep_b200.csv")
     ap.add_argument("--report", default=None, help="JSON summary path")
     ap.add_argument("--tolerance", type=float, default=0.04)
+    ap.add_argument("--depth", action="store_true",
+                    help="sweep R = 0..4 (sweep_r) at the Table II sizes instead of m")
     a = ap.parse_args(argv)
+    if a.depth:
+        return main_depth(a)
     sizes = TABLE1_SIZES if a.sizes == "table1" else [int(float(s)) for s in a.sizes.split(",")]
     cands = [int(c) for c in a.candidates.split(",")]
     model = default_size_model()
@@ -287,6 +291,35 @@ def main(argv=None):
         with open(a.report, "w") as f:
             json.dump(summary, f, indent=1)
     print(f"kNN (RTX 2080 Ti model) == B200 argmin at {summary['argmin_equals_knn']}/{len(rows)} sizes")
+
+
+# the paper's Table II sizes (depth model training data)
+TABLE2_SIZES = [100000, 1000000, 2000000, 2200000, 2300000, 2400000, 2500000, 3000000, 4000000,
+                4500000, 4800000, 5000000, 8000000, 8400000, 9200000, 9600000, 10000000, 100000000]
+
+
+def main_depth(a):
+    """sweep_r over R = 0..4 with the bundled size model; compares the B200
+    argmin depth with the depth model's prediction (fit_depth_model, Table II)."""
+    from .tridpart import default_depth_model
+
+    sizes = TABLE2_SIZES if a.sizes == "table1" else [int(float(s)) for s in a.sizes.split(",")]
+    size_model, depth_model = default_size_model(), default_depth_model()
+    obs = ObservationSet()
+    rows = []
+    for n in sizes:
+        res = sweep_r(n, kMaxRecursionDepth, size_model, a.runs, a.seed)
+        o = res.to_observation()
+        obs.rows.append(o)
+        pred = predict(depth_model, n)
+        rows.append({"n": n, "argmin_R": res.argmin, "times_ms": o.times, "knn_R": pred})
+        print(f"N={n:>10}  argmin R={res.argmin}  times " +
+              " ".join(f"R{r}={t:.4f}" for r, t in sorted(o.times.items())) + f"  kNN R={pred}", flush=True)
+    write_observations(obs, a.out)
+    if a.report:
+        with open(a.report, "w") as f:
+            json.dump({"device": "b200", "runs": a.runs, "rows": rows,
+                       "argmin_equals_knn": sum(1 for r in rows if r["argmin_R"] == r["knn_R"])}, f, indent=1)
 
 
 if __name__ == "__main__":
