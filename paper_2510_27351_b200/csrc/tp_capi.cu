@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -300,7 +301,7 @@ struct Runner {
 
     // Whole solve: reset the error word, Stage 1 down, finish, Stage 3 up.
     void solve(const Plan<T>& p) {
-        check(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
+        check(tpb::launch_reset(ctx->d_err, st));
         solve_body(p);
     }
     void solve_body(const Plan<T>& p) {
@@ -311,7 +312,7 @@ struct Runner {
 
     // Sharded halves.
     void shard_reduce(const Plan<T>& p, T* eq8) {
-        check(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), st));
+        check(tpb::launch_reset(ctx->d_err, st));
         for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
         IfacePtrs<T> o{eq8, eq8 + 2, eq8 + 4, eq8 + 6};
         check(tpb::launch_final<T>(tpb::kStage1, p.final_in, p.n_final, o, nullptr, nullptr, ctx->d_err,

@@ -78,6 +78,15 @@ struct MinGuard {
     __device__ __forceinline__ bool tripped() const { return pmin < pivot_floor<T>(); }
 };
 
+// Programmatic dependent launch. Every solve-path kernel starts with this:
+// wait until the preceding grid in the stream has completed and its writes are
+// visible (a no-op when launched without the PDL attribute), then let the next
+// grid start launching so its CTAs are resident when this one drains.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // err word encodes (level << 48) | row; atomicMin keeps the lexicographically
 // first failure. Reported to the host as ZeroPivotError(row) at `level`.
 __device__ __forceinline__ void report_pivot(unsigned long long* err, int level, int64_t bad) {

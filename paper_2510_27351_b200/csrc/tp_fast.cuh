@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int lane = threadIdx.x & 31;
     const int c = lane % G;  // chunk index inside the block
     int64_t bad = INT64_MAX;
+    pdl_begin();
 
     for (int64_t base = (int64_t)blockIdx.x * THREADS; base < nchunks;
          base += (int64_t)gridDim.x * THREADS) {
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
     const int len = llo + (c < ext ? 1 : 0);
     const int off = c * llo + (c < ext ? c : ext);
     int64_t bad = INT64_MAX;
+    pdl_begin();
 
     for (int64_t base = (int64_t)blockIdx.x * THREADS; base < nchunks;
          base += (int64_t)gridDim.x * THREADS) {

@@ -11,6 +11,7 @@
 //   k_generate           device-side counter-based generate_system analogue
 //   k_residual           residual_inf (tridiagonal.hpp:74-87)
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "tp_device.cuh"
@@ -18,6 +19,19 @@
 #include "tp_fast.cuh"
 
 namespace tpb {
+
+// Phase timestamps of the finishing solve (scratch builds with -DTPB_TRACE only).
+#ifdef TPB_TRACE
+__device__ unsigned long long g_trace[16];
+#define TP_TRACE_DECL long long tp_tr[12]
+#define TP_TRACE(k) tp_tr[k] = clock64()
+#define TP_TRACE_FLUSH \
+    do { if (threadIdx.x == 0) for (int k_ = 0; k_ < 12; ++k_) g_trace[k_] = tp_tr[k_]; } while (0)
+#else
+#define TP_TRACE_DECL
+#define TP_TRACE(k) do { } while (0)
+#define TP_TRACE_FLUSH do { } while (0)
+#endif
 
 // ===========================================================================
 // Generic path: any block length, rows staged through shared memory.
@@ -108,6 +122,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs<T> sys, int64
     while ((1 << logg) < G) ++logg;
     RowGuard bad;
     constexpr bool KEEP = (MODE != kStage1);
+    pdl_begin();
 
     const int64_t ntiles = (nblocks + bpc - 1) / bpc;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -252,6 +267,9 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
     __shared__ T wx[2 * (kFinalThreads2 / 32)];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     RowGuard bad;
+    TP_TRACE_DECL;
+    pdl_begin();
+    TP_TRACE(0);
 
     if (n == 1) {  // thomas_solve on one row (tridiagonal.hpp:57-59)
         if (tid == 0 && MODE == kSolve) {
@@ -289,6 +307,7 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
         }
     }
     __syncthreads();
+    TP_TRACE(1);
 
     const int Llo = (int)(n / G), ext = (int)(n % G);
     const bool active = tid < G;
@@ -299,6 +318,7 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
 
     Eq2<T> cur = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
     if (active) cur = leaf_smem<T, KEEP>(sa + off, sb + off, sc + off, sd + off, len, off, bad);
+    TP_TRACE(2);
 
     // ---- warp-level tree (chunk index == tid) ----
     MergeSave<T> sw[5];
@@ -311,7 +331,9 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
     }
     const int nwr = G >= 32 ? G / 32 : 1;  // warp roots
     if (lane == 0 && warp < nwr) wroot[warp] = cur;
+    TP_TRACE(3);
     __syncthreads();
+    TP_TRACE(4);
 
     // ---- warp 0: merge the warp roots, handle the root, push ends back down ----
     if (warp == 0) {
@@ -324,6 +346,7 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
             if (h < nwr && (lane & (2 * h - 1)) == 0 && lane + h < nwr)
                 wc = merge(wc, oth, (int64_t)chunk_start(32 * (lane + h)) - 1, bad, sx[lv]);
         }
+        TP_TRACE(5);
         T xs = 0, xe = 0;
         if (lane == 0) {
             if (MODE == kStage1) {
@@ -359,12 +382,14 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
                 wx[2 * lane + 1] = xe;
             }
         }
+        TP_TRACE(6);
     }
     if (MODE == kStage1) {
         report_pivot(err, level, bad.bad);
         return;
     }
     __syncthreads();
+    TP_TRACE(7);
 
     // ---- every warp: its segment ends, then the warp-level tree top-down ----
     T xs = 0, xe = 0;
@@ -387,6 +412,7 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
             xe = xt;
         }
     }
+    TP_TRACE(8);
     // ---- leaf back-substitution into the a-slots, then a coalesced store ----
     if (active) {
         T* a = sa + off;
@@ -402,8 +428,12 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
         a[0] = xs;
         a[len - 1] = xe;
     }
+    TP_TRACE(9);
     __syncthreads();
+    TP_TRACE(10);
     for (int64_t i = tid; i < n; i += kFinalThreads2) x[i] = sa[i];
+    TP_TRACE(11);
+    TP_TRACE_FLUSH;
     report_pivot(err, level, bad.bad);
 }
 
@@ -417,6 +447,7 @@ template <class T>
 __global__ void k_gather_solve(const T* __restrict__ eqs, int nranks, int rank,
                                T* __restrict__ x2, T* __restrict__ scratch,
                                unsigned long long* err, int level) {
+    pdl_begin();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int n = 2 * nranks;
     T* cm = scratch;
@@ -443,13 +474,6 @@ __global__ void k_gather_solve(const T* __restrict__ eqs, int nranks, int rank,
     report_pivot(err, level, bad.bad);
 }
 
-// ===========================================================================
-// Device generator: same distributions as generate_system (bench.hpp:68-93)
-// — a,c,d ~ U[-1,1), b = delta*(|a|+|c|)+1, whole-row sign flip with p=0.5,
-// sub[0] = super[N-1] = 0 — from a counter-based hash of (seed, global row),
-// so any shard generates its slice of the same global system. NOT
-// bit-identical to std::mt19937_64; used for throughput runs only.
-// ===========================================================================
 // ===========================================================================
 // Device generator: same distributions as generate_system (bench.hpp:68-93)
 // — a,c,d ~ U[-1,1), b = delta*(|a|+|c|)+1, whole-row sign flip with p=0.5,
@@ -516,6 +540,42 @@ __global__ void k_residual(SysPtrs<T> sys, int64_t n, const T* __restrict__ x, u
 // Launchers
 // ===========================================================================
 
+// Launch policy, fixed once by init_kernel_attributes(): with TPB_PDL=1 the
+// solve-path kernels go out with the programmatic-stream-serialization
+// attribute (PDL; inside a captured graph the edges become programmatic
+// edges). Every such kernel begins with pdl_begin(), so it is correct either
+// way. Off by default: measured on B200 (tools/timeline.py, C3) it saves ~6 us
+// across the levels >= 1 but the persistent Stage-3 grid launched early
+// behind level 1 runs ~50 us slower.
+static bool g_pdl = false;
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                            cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// Error-word reset at the head of every solve (a kernel rather than a memset
+// node, so the first Stage-1 grid can be launched programmatically after it).
+__global__ void k_reset(unsigned long long* err) {
+    pdl_begin();
+    if (threadIdx.x == 0) *err = kNoError;
+}
+
+cudaError_t launch_reset(unsigned long long* err, cudaStream_t st) {
+    return launch_k(k_reset, 1, 32, 0, st, err);
+}
+
 // Launch shapes chosen by measurement (scratch/tune.cu on B200, N=1e8, m=64):
 // Stage 1  128 threads, <=80 regs (6 CTAs/SM), one chunk per thread (full grid)
 // Stage 3  128 threads, <=128 regs (4 CTAs/SM), persistent grid-stride
@@ -535,17 +595,16 @@ static cudaError_t launch_fast_t(int mode, const SysPtrs<T>& sys, int64_t nblock
         using C = FastCfg<T, L, G, kStage1, VEC>;
         int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
         if (grid < 1) grid = 1;
-        k_fast<T, L, G, kStage1, VEC, C::kThreads, C::kMinBlocks><<<(unsigned)grid, C::kThreads, 0, st>>>(
-            sys, nblocks, out, xi, x, err, level);
+        return launch_k(k_fast<T, L, G, kStage1, VEC, C::kThreads, C::kMinBlocks>, (unsigned)grid,
+                        C::kThreads, 0, st, sys, nblocks, out, xi, x, err, level);
     } else {
         using C = FastCfg<T, L, G, kStage3, VEC>;
         int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
         if (grid > grid_cap) grid = grid_cap;
         if (grid < 1) grid = 1;
-        k_fast<T, L, G, kStage3, VEC, C::kThreads, C::kMinBlocks><<<(unsigned)grid, C::kThreads, 0, st>>>(
-            sys, nblocks, out, xi, x, err, level);
+        return launch_k(k_fast<T, L, G, kStage3, VEC, C::kThreads, C::kMinBlocks>, (unsigned)grid,
+                        C::kThreads, 0, st, sys, nblocks, out, xi, x, err, level);
     }
-    return cudaGetLastError();
 }
 
 template <class T, int L, int G>
@@ -636,10 +695,8 @@ cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs<T>& sys, int64_t n
 #define TPB_RT(GG)                                                                                     \
     case GG:                                                                                           \
         if (mode == kStage1)                                                                           \
-            k_fast_rt<T, 8, GG, kStage1><<<(unsigned)grid, 128, 0, st>>>(sys, nblocks, m, out, xi, x, err, level); \
-        else                                                                                           \
-            k_fast_rt<T, 8, GG, kStage3><<<(unsigned)grid, 128, 0, st>>>(sys, nblocks, m, out, xi, x, err, level); \
-        break;
+            return launch_k(k_fast_rt<T, 8, GG, kStage1>, (unsigned)grid, 128, 0, st, sys, nblocks, m, out, xi, x, err, level); \
+        return launch_k(k_fast_rt<T, 8, GG, kStage3>, (unsigned)grid, 128, 0, st, sys, nblocks, m, out, xi, x, err, level);
     switch (G) {
         TPB_RT(1)
         TPB_RT(2)
@@ -650,7 +707,6 @@ cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs<T>& sys, int64_t n
         default: return cudaErrorInvalidValue;
     }
 #undef TPB_RT
-    return cudaGetLastError();
 }
 
 size_t generic_smem_bytes(int threads, int G, int64_t blen, size_t elem) {
@@ -666,14 +722,9 @@ cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs
                            int level, cudaStream_t st) {
     const size_t smem = generic_smem_bytes(threads, G, blen, sizeof(T));
     if (smem > kMaxDynSmem) return cudaErrorInvalidValue;
-    if (mode == kStage1) {
-        k_generic<T, kStage1><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
-    } else if (mode == kStage3) {
-        k_generic<T, kStage3><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
-    } else {
-        k_generic<T, kSolve><<<grid, threads, smem, st>>>(sys, row_base, blk_base, nblocks, blen, G, out, xi, x, err, level);
-    }
-    return cudaGetLastError();
+    auto k = mode == kStage1 ? k_generic<T, kStage1> : mode == kStage3 ? k_generic<T, kStage3> : k_generic<T, kSolve>;
+    return launch_k(k, (unsigned)grid, (unsigned)threads, smem, st, sys, row_base, blk_base, nblocks, blen, G,
+                    out, xi, x, err, level);
 }
 
 static int final_G(int64_t n) {
@@ -688,13 +739,8 @@ cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const Iface
     if (n > kFinalCap || n < 1) return cudaErrorInvalidValue;
     const int G = final_G(n);
     const size_t smem = (size_t)(4 * n) * sizeof(T);
-    if (mode == kStage1)
-        k_final<T, kStage1><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
-    else if (mode == kStage3)
-        k_final<T, kStage3><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
-    else
-        k_final<T, kSolve><<<1, kFinalThreads2, smem, st>>>(sys, n, G, out, xi, x, err, level);
-    return cudaGetLastError();
+    auto k = mode == kStage1 ? k_final<T, kStage1> : mode == kStage3 ? k_final<T, kStage3> : k_final<T, kSolve>;
+    return launch_k(k, 1, kFinalThreads2, smem, st, sys, n, G, out, xi, x, err, level);
 }
 
 template <class T>
@@ -709,17 +755,36 @@ static cudaError_t set_smem_attributes() {
     return e;
 }
 
+// Experiment switch TPB_CARVEOUT=<percent>: preferred shared-memory carveout
+// of the register-path kernels (by default the driver picks one per kernel).
+template <class T>
+static cudaError_t set_carveout(int pct) {
+    cudaError_t e = cudaSuccess;
+#define TPB_CO(MM, LL, GG)                                                                              \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(FastCfg<T, LL, GG, kStage1, true>::fn(), cudaFuncAttributePreferredSharedMemoryCarveout, pct);  \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(FastCfg<T, LL, GG, kStage1, false>::fn(), cudaFuncAttributePreferredSharedMemoryCarveout, pct); \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(FastCfg<T, LL, GG, kStage3, true>::fn(), cudaFuncAttributePreferredSharedMemoryCarveout, pct);  \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(FastCfg<T, LL, GG, kStage3, false>::fn(), cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    TPB_FAST_SHAPES(TPB_CO)
+#undef TPB_CO
+    return e;
+}
+
 cudaError_t init_kernel_attributes() {
+    if (const char* v = getenv("TPB_PDL")) g_pdl = atoi(v) != 0;
     cudaError_t e = set_smem_attributes<double>();
     if (e == cudaSuccess) e = set_smem_attributes<float>();
+    if (const char* v = getenv("TPB_CARVEOUT")) {
+        if (e == cudaSuccess) e = set_carveout<double>(atoi(v));
+        if (e == cudaSuccess) e = set_carveout<float>(atoi(v));
+    }
     return e;
 }
 
 template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st) {
-    k_gather_solve<T><<<1, 32, 0, st>>>(eqs, nranks, rank, x2, scratch, err, level);
-    return cudaGetLastError();
+    return launch_k(k_gather_solve<T>, 1, 32, 0, st, eqs, nranks, rank, x2, scratch, err, level);
 }
 
 template <class T>
@@ -787,6 +852,12 @@ __global__ void k_diag_rcp(int64_t n, uint64_t seed, unsigned long long* max_ulp
     atomicMax(max_ulp, worst);
 }
 }  // namespace tpb
+
+#ifdef TPB_TRACE
+extern "C" int tp_debug_trace(uint64_t* out) {
+    return cudaMemcpyFromSymbol(out, tpb::g_trace, sizeof(tpb::g_trace)) == cudaSuccess ? 0 : 9;
+}
+#endif
 
 extern "C" int tp_diag_rcp_ulp(int64_t n, uint64_t seed, uint64_t* max_ulp) {
     unsigned long long* d = nullptr;

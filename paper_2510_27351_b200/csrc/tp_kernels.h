@@ -38,6 +38,7 @@ struct IfacePtrs {
 };
 
 cudaError_t init_kernel_attributes();
+cudaError_t launch_reset(unsigned long long* err, cudaStream_t st);
 bool fast_shape(int64_t m, int* L, int* G);
 int fast_rt_G(int64_t m);
 
