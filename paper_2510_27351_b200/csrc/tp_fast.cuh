@@ -110,6 +110,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
         const int64_t blk = t / G;
         LaneState<T, L, G, KEEP> s;
         load_chunk<T, L, VEC>(sys, row0, active, s.r);
+        // Stage 3: the block's ends from the next level's solution, issued with
+        // the row loads so its latency is off the sweep -> tree -> expand chain
+        T xs = 0, xe = 0;
+        if constexpr (MODE != kStage1) {
+            if (c == 0 && active) {
+                const Pair<T> v = load_pair(xi + 2 * blk);
+                xs = v.x;
+                xe = v.y;
+            }
+        }
         lane_leaf<T, L, G, KEEP>(s, row0);
         lanes_tree<T, L, G, KEEP>(s, c, row0);
         if constexpr (MODE == kStage1) {
@@ -118,13 +128,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 if (c == 0) store_block_eqs(out, blk, s.cur);
             }
         } else {
-            // block ends from the next level's solution
-            T xs = 0, xe = 0;
-            if (c == 0 && active) {
-                const Pair<T> v = load_pair(xi + 2 * blk);
-                xs = v.x;
-                xe = v.y;
-            }
             T xv[L];
             lanes_tree_down<T, L, G>(s, c, xs, xe);
             leaf_expand<T, L, L>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv);
@@ -165,6 +168,14 @@ __global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
         const int64_t blk = t / G;
         const int64_t row0 = blk * m + off;
         LaneState<T, LMAX, G, KEEP> s;
+        T xs = 0, xe = 0;  // Stage 3 block ends, loaded with the rows (see k_fast)
+        if constexpr (MODE != kStage1) {
+            if (c == 0 && active) {
+                const Pair<T> v = load_pair(xi + 2 * blk);
+                xs = v.x;
+                xe = v.y;
+            }
+        }
 #pragma unroll
         for (int i = 0; i < LMAX; ++i) {
             const bool live = active && i < len;
@@ -191,12 +202,6 @@ __global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
                 if (c == 0) store_block_eqs(out, blk, s.cur);
             }
         } else {
-            T xs = 0, xe = 0;
-            if (c == 0 && active) {
-                const Pair<T> v = load_pair(xi + 2 * blk);
-                xs = v.x;
-                xe = v.y;
-            }
             T xv[LMAX];
             lanes_tree_down<T, LMAX, G>(s, c, xs, xe);
             switch (len) {
