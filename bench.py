@@ -47,7 +47,10 @@ def parse():
     p.add_argument("--cpu-runs", type=int, default=3)
     p.add_argument("--prewarm", type=float, default=0.3, help="seconds of untimed solves before warm-up")
     p.add_argument("--force-sharded", action="store_true",
-                   help="run the multi-GPU code path (NCCL all-gather) even with one rank")
+                   help="run the multi-GPU code path even with one rank")
+    p.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
+                   help="multi-GPU exchange: fused peer-memory (p2p), NCCL all-gather, or p2p with "
+                        "NCCL fallback (auto)")
     return p.parse_args()
 
 
@@ -213,6 +216,11 @@ def run_ours(args):
     sharded_mode = world > 1 or args.force_sharded
     if sharded_mode:
         import torch.distributed as dist
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"  # keep rank 0's stdout to the one JSON line
+        if "RANK" not in os.environ:  # --force-sharded without torchrun: a 1-rank group
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_per = int(args.n)
     n_glob = n_per * world
@@ -229,7 +237,7 @@ def run_ours(args):
         def step():
             tp.solve_partition_async(sys_d, policy, out=x)
     else:
-        solver = sharded.ShardedSolver()
+        solver = sharded.ShardedSolver(transport=args.transport)
 
         def step():
             solver.solve(sys4, n_glob, policy, out=x)
@@ -338,8 +346,7 @@ def run_ours(args):
                   C.c_void_p(hx[0].data_ptr()))
             sync_ms = (time.perf_counter() - t0) * 1e3
         else:
-            dsys = [torch.empty_like(t) for t in sys4]
-            solver = sharded.ShardedSolver()
+            dsys = [torch.empty_like(t) for t in sys4]  # same solver (and peer links) as above
 
             def e2e_run(k):
                 for _ in range(k):
@@ -409,7 +416,12 @@ def run_ours(args):
             "config": {"workload": "recursive partition solve, kNN policy, N=1e8 per GPU (config 3)",
                        "n_per_gpu": n_per, "n_global": n_glob, "policy": policy.sizes,
                        "l2": "inputs 3.2 GB/GPU >> 126 MB L2 (no flush)",
-                       "parallelism": "single GPU" if not sharded_mode else f"{world} contiguous shard(s) + NCCL all-gather"},
+                       "parallelism": "single GPU" if not sharded_mode else (
+                           f"{world} contiguous shard(s) + " + (
+                               "fused peer-memory exchange in the finishing kernel (CUDA IPC)"
+                               if solver.transport == "p2p" else "NCCL all-gather")),
+                       "transport": None if not sharded_mode else solver.transport,
+                       "transport_fallback": None if not sharded_mode else solver.fallback_reason},
             "hbm": {"solve_GBps_40B_per_gpu": solve_gbs,
                     "frac_40B": solve_gbs / peak,
                     "frac_72B": solve_gbs * TWO_PASS_BYTES_PER_UNKNOWN / ALG_BYTES_PER_UNKNOWN / peak,

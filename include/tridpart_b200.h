@@ -46,7 +46,7 @@ typedef enum tp_status {
     TP_ERR_IO = 8,                  /* Error("cannot open ...")     io.hpp:80-84     */
     TP_ERR_CUDA = 9,                /* device / runtime failure (no reference analogue) */
     TP_ERR_INVALID_ARGUMENT = 10,   /* NULL pointer, bad rank, ... */
-    TP_ERR_NCCL = 11                /* reserved for the collective path */
+    TP_ERR_NCCL = 11                /* collective path: peer exchange timed out, ... */
 } tp_status;
 
 typedef struct tp_error {
@@ -158,6 +158,34 @@ tp_status tp_shard_finish_f64_dev(tp_ctx* ctx, const double* sub, const double* 
                                   const int64_t* sizes, int32_t nsizes, const double* eq_all_dev,
                                   int32_t nranks, int32_t rank, double* x_dev, void* stream,
                                   tp_error* err);
+
+/* Fused multi-GPU solve (the collective inside the kernel, no NCCL call):
+ * every rank allocates a mailbox (tp_shard_mailbox), exports it with
+ * tp_ipc_get_handle, opens every peer's with tp_ipc_open_handle (CUDA IPC:
+ * peer memory over NVLink/NVSwitch; same-process peers pass raw pointers),
+ * then calls tp_shard_attach with all P mailboxes in rank order and a barrier
+ * across ranks. tp_shard_solve_f64_dev then runs the whole shard solve as one
+ * captured graph: Stage 1 levels -> a single-CTA kernel that reduces the shard
+ * to its boundary pair, stores it into every peer's mailbox, waits for all P
+ * pairs (bounded spin; timeout -> TP_ERR_NCCL), solves the 2P-row top system
+ * (Thomas) and expands -> Stage 3 levels. All ranks must call it the same
+ * number of times (the epoch flags pair the calls). */
+tp_status tp_shard_mailbox(tp_ctx* ctx, int32_t nranks, void** mailbox, tp_error* err);
+tp_status tp_ipc_get_handle(tp_ctx* ctx, void* dev_ptr, uint8_t* handle64, tp_error* err);
+tp_status tp_ipc_open_handle(tp_ctx* ctx, const uint8_t* handle64, void** dev_ptr, tp_error* err);
+tp_status tp_shard_attach(tp_ctx* ctx, int32_t nranks, int32_t rank, void* const* mailboxes,
+                          tp_error* err);
+tp_status tp_shard_solve_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                 const double* super, const double* rhs, int64_t n_local,
+                                 const int64_t* sizes, int32_t nsizes, double* x_dev, void* stream,
+                                 tp_error* err);
+/* Same arguments: capture and instantiate the solve's graph without launching
+ * it (graph instantiation can wait for the device to go idle, so ranks that
+ * share one GPU prepare every graph before any rank's exchange is in flight). */
+tp_status tp_shard_prepare_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
+                                   const double* super, const double* rhs, int64_t n_local,
+                                   const int64_t* sizes, int32_t nsizes, double* x_dev, void* stream,
+                                   tp_error* err);
 
 /* --------------------------------------------------- synthetic inputs */
 /* Device analogue of generate_system(n, seed, delta) — bench.hpp:68-93: same

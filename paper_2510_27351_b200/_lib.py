@@ -43,7 +43,8 @@ EXPORTS = [
     "tp_obs_get", "tp_obs_free", "tp_diag_rcp_ulp", "tp_solve_partition_f32",
     "tp_solve_partition_f32_dev", "tp_solve_partition_observe_f32", "tp_thomas_solve_f32",
     "tp_residual_inf_f32_dev", "tp_generate_system_f32_dev", "tp_solve_partition_f64_async",
-    "tp_solve_partition_f32_async",
+    "tp_solve_partition_f32_async", "tp_shard_mailbox", "tp_ipc_get_handle", "tp_ipc_open_handle",
+    "tp_shard_attach", "tp_shard_solve_f64_dev", "tp_shard_prepare_f64_dev",
 ]
 
 
@@ -99,6 +100,12 @@ def _load():
         "tp_solve_partition_f32_async": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
                                                    vp, E]),
         "tp_residual_inf_f32_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, _D, E]),
+        "tp_shard_mailbox": (C.c_int, [vp, C.c_int32, C.POINTER(vp), E]),
+        "tp_ipc_get_handle": (C.c_int, [vp, vp, C.POINTER(C.c_uint8), E]),
+        "tp_ipc_open_handle": (C.c_int, [vp, C.POINTER(C.c_uint8), C.POINTER(vp), E]),
+        "tp_shard_attach": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp), E]),
+        "tp_shard_solve_f64_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp, vp, E]),
+        "tp_shard_prepare_f64_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp, vp, E]),
         "tp_generate_system_f32_dev": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
                                                  C.c_double, vp, vp, vp, vp, vp, E]),
     }

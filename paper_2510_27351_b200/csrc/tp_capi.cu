@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -191,6 +192,15 @@ struct tp_ctx {
     unsigned long long* h_err = nullptr;
     unsigned long long* d_red = nullptr;  // residual / scratch words
     void* d_small = nullptr;              // shard scratch (x2 + gather scratch)
+    // fused multi-GPU path (k_final<kShard>): own mailbox, peer links, epoch word
+    void* mailbox = nullptr;
+    int mailbox_ranks = 0;
+    unsigned long long* d_epoch = nullptr;
+    tpb::ShardLink link{};
+    bool linked = false;
+    int64_t link_gen = 0;
+    std::vector<void*> ipc_opened;
+    bool prepare_only = false;  // capture + instantiate the graph, do not launch
     void* dsys = nullptr;                 // host-path staging (5 arrays)
     size_t dsys_cap = 0;                  // bytes
     int64_t last_launches = 0;
@@ -319,6 +329,16 @@ struct Runner {
                                    (int)p.levels.size(), st));
         after("shard_reduce", (int)p.levels.size());
     }
+    // Fused multi-GPU solve of one shard: every local level, the peer exchange
+    // and top solve inside the finishing kernel, every local Stage 3.
+    void shard_solve(const Plan<T>& p) {
+        check(tpb::launch_reset(ctx->d_err, st));
+        for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
+        check(tpb::launch_final<T>(tpb::kShard, p.final_in, p.n_final, IfacePtrs<T>{}, nullptr, p.final_x,
+                                   ctx->d_err, (int)p.levels.size(), st, &ctx->link));
+        after("shard_exchange", (int)p.levels.size());
+        for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
+    }
     void shard_finish(const Plan<T>& p, const T* eq_all, int nranks, int rank) {
         T* x2 = static_cast<T*>(ctx->d_small);
         T* scratch = x2 + 32;
@@ -401,6 +421,10 @@ tp_status decode_device_error(tp_ctx* ctx, tp_error* err) {
     if (code == tpb::kNoError) return TP_OK;
     const int32_t level = (int32_t)(code >> 48);
     const int64_t row = (int64_t)(code & 0xFFFFFFFFFFFFULL);
+    if (level == tpb::kExchangeLevel) {
+        set_err(err, TP_ERR_NCCL, "peer exchange timed out waiting for rank " + std::to_string(row), row, -1);
+        return TP_ERR_NCCL;
+    }
     set_err(err, TP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(row), row, level);
     return TP_ERR_ZERO_PIVOT;
 }
@@ -422,7 +446,7 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
     for (auto& g : ctx->gcache) {
         if (g.key == key) {
             g.stamp = ++ctx->clock;
-            TP_CUDA(cudaGraphLaunch(g.exec, st));
+            if (!ctx->prepare_only) TP_CUDA(cudaGraphLaunch(g.exec, st));
             ctx->last_launches = g.launches;
             return TP_OK;
         }
@@ -434,11 +458,16 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
         TP_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
         own_cap = true;
     }
+    static const bool dbg = getenv("TPB_DEBUG_GRAPH") != nullptr;
+    auto now_ms = [] { return std::chrono::duration<double, std::milli>(
+                           std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t0 = dbg ? now_ms() : 0;
     TP_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     Runner<T> r{ctx, cap};
     fn(r);
     cudaGraph_t graph = nullptr;
     cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+    const double t1 = dbg ? now_ms() : 0;
     if (r.status != cudaSuccess || ce != cudaSuccess) {
         if (graph) cudaGraphDestroy(graph);
         if (own_cap) cudaStreamDestroy(cap);
@@ -451,6 +480,7 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
     cudaGraphExec_t exec = nullptr;
     cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
+    const double t2 = dbg ? now_ms() : 0;
     if (ie != cudaSuccess) {
         set_err(err, TP_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
         return TP_ERR_CUDA;
@@ -468,7 +498,10 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
     ge.stamp = ++ctx->clock;
     ctx->gcache.push_back(ge);
     ctx->last_launches = r.launches;
-    TP_CUDA(cudaGraphLaunch(exec, st));
+    if (!ctx->prepare_only) TP_CUDA(cudaGraphLaunch(exec, st));
+    if (dbg)
+        std::fprintf(stderr, "[tpb graph] capture %.3f ms, instantiate %.3f ms, launch %.3f ms (%lld kernels)\n",
+                     t1 - t0, t2 - t1, now_ms() - t2, (long long)r.launches);
     return TP_OK;
 }
 
@@ -713,6 +746,35 @@ tp_status shard_finish(tp_ctx* ctx, const T* sub, const T* diag, const T* super,
 }
 
 template <class T>
+tp_status shard_solve(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs, int64_t n_local,
+                      const int64_t* sizes, int32_t nsizes, T* x_dev, void* stream, tp_error* err) {
+    clear_err(err);
+    if (!ctx) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    if (!ctx->linked) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "no peer links: call tp_shard_attach first");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    tp_status s = validate(sub, diag, super, rhs, n_local, sizes, nsizes, x_dev, err);
+    if (s != TP_OK) return s;
+    if (n_local < 2) {
+        set_err(err, TP_ERR_INVALID_SIZE, "a shard needs at least 2 rows");
+        return TP_ERR_INVALID_SIZE;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    Plan<T> p;
+    build_plan(n_local, sizes, nsizes, p);
+    s = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
+    if (s != TP_OK) return s;
+    bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, x_dev, ctx->ws);
+    const cudaStream_t st = pick_stream(ctx, stream);
+    auto key = make_key<T>(5, n_local, sizes, nsizes, {sub, diag, super, rhs, x_dev, ctx->ws}, ctx->link_gen);
+    return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.shard_solve(p); }, err);
+}
+
+template <class T>
 tp_status generate_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global, uint64_t seed, double delta,
                        T* sub, T* diag, T* super, T* rhs, void* stream, tp_error* err) {
     clear_err(err);
@@ -811,6 +873,9 @@ void tp_ctx_destroy(tp_ctx* ctx) {
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->d_red) cudaFree(ctx->d_red);
     if (ctx->d_small) cudaFree(ctx->d_small);
+    for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (ctx->mailbox) cudaFree(ctx->mailbox);
+    if (ctx->d_epoch) cudaFree(ctx->d_epoch);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -925,6 +990,117 @@ tp_status tp_shard_finish_f64_dev(tp_ctx* ctx, const double* sub, const double* 
                                   tp_error* err) {
     return shard_finish<double>(ctx, sub, diag, super, rhs, n_local, sizes, nsizes, eq_all_dev, nranks,
                                 rank, x_dev, stream, err);
+}
+
+tp_status tp_shard_solve_f64_dev(tp_ctx* ctx, const double* sub, const double* diag, const double* super,
+                                 const double* rhs, int64_t n_local, const int64_t* sizes, int32_t nsizes,
+                                 double* x_dev, void* stream, tp_error* err) {
+    return shard_solve<double>(ctx, sub, diag, super, rhs, n_local, sizes, nsizes, x_dev, stream, err);
+}
+
+tp_status tp_shard_prepare_f64_dev(tp_ctx* ctx, const double* sub, const double* diag, const double* super,
+                                   const double* rhs, int64_t n_local, const int64_t* sizes, int32_t nsizes,
+                                   double* x_dev, void* stream, tp_error* err) {
+    if (!ctx) return shard_solve<double>(ctx, sub, diag, super, rhs, n_local, sizes, nsizes, x_dev, stream, err);
+    if (!ctx->graphs) {
+        clear_err(err);
+        return TP_OK;  // nothing to prepare without graphs
+    }
+    ctx->prepare_only = true;
+    const tp_status s = shard_solve<double>(ctx, sub, diag, super, rhs, n_local, sizes, nsizes, x_dev, stream, err);
+    ctx->prepare_only = false;
+    return s;
+}
+
+tp_status tp_shard_mailbox(tp_ctx* ctx, int32_t nranks, void** mailbox, tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    if (!mailbox || nranks < 1 || nranks > tpb::kMaxPeers) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "mailbox: bad arguments (1..64 ranks)");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    if (ctx->mailbox && ctx->mailbox_ranks != nranks) {
+        TP_CUDA(cudaDeviceSynchronize());
+        TP_CUDA(cudaFree(ctx->mailbox));
+        ctx->mailbox = nullptr;
+        ctx->linked = false;
+    }
+    if (!ctx->mailbox) {
+        // its own allocation, so a CUDA IPC handle of it maps exactly the mailbox
+        TP_CUDA(cudaMalloc(&ctx->mailbox, tpb::mailbox_bytes(nranks)));
+        TP_CUDA(cudaMemset(ctx->mailbox, 0, tpb::mailbox_bytes(nranks)));
+        ctx->mailbox_ranks = nranks;
+    }
+    if (!ctx->d_epoch) {
+        TP_CUDA(cudaMalloc(&ctx->d_epoch, 256));
+        TP_CUDA(cudaMemset(ctx->d_epoch, 0, 256));
+    }
+    *mailbox = ctx->mailbox;
+    return TP_OK;
+}
+
+tp_status tp_ipc_get_handle(tp_ctx* ctx, void* dev_ptr, uint8_t* handle64, tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    if (!dev_ptr || !handle64) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    cudaIpcMemHandle_t h;
+    TP_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, 64);
+    return TP_OK;
+}
+
+tp_status tp_ipc_open_handle(tp_ctx* ctx, const uint8_t* handle64, void** dev_ptr, tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    if (!dev_ptr || !handle64) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    TP_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->ipc_opened.push_back(*dev_ptr);
+    return TP_OK;
+}
+
+tp_status tp_shard_attach(tp_ctx* ctx, int32_t nranks, int32_t rank, void* const* mailboxes, tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    if (!mailboxes || nranks < 1 || nranks > tpb::kMaxPeers || rank < 0 || rank >= nranks) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "attach: bad rank / nranks (1..64 ranks)");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    if (!ctx->mailbox || ctx->mailbox_ranks != nranks || mailboxes[rank] != ctx->mailbox) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "attach: mailboxes[rank] must be this context's tp_shard_mailbox");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    for (int p = 0; p < nranks; ++p)
+        if (!mailboxes[p]) {
+            set_err(err, TP_ERR_INVALID_ARGUMENT, "attach: null peer mailbox");
+            return TP_ERR_INVALID_ARGUMENT;
+        }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    TP_CUDA(cudaDeviceSynchronize());
+    TP_CUDA(cudaMemset(ctx->mailbox, 0, tpb::mailbox_bytes(nranks)));
+    TP_CUDA(cudaMemset(ctx->d_epoch, 0, 256));
+    TP_CUDA(cudaDeviceSynchronize());
+    tpb::ShardLink lk{};
+    for (int p = 0; p < nranks; ++p) lk.peers[p] = static_cast<double*>(mailboxes[p]);
+    lk.own = static_cast<double*>(ctx->mailbox);
+    lk.epoch = ctx->d_epoch;
+    lk.nranks = nranks;
+    lk.rank = rank;
+    ctx->link = lk;
+    ctx->linked = true;
+    ++ctx->link_gen;  // graphs captured with the previous links stay keyed to them
+    return TP_OK;
 }
 
 // ---- synthetic inputs -----------------------------------------------------

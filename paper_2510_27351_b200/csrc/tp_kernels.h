@@ -11,6 +11,8 @@ namespace tpb {
 constexpr int kStage1 = 0;  // reduce blocks -> next level's interface rows
 constexpr int kStage3 = 1;  // expand blocks from the next level's solution
 constexpr int kSolve = 2;   // whole system as one block: reduce, 2x2 root, expand
+constexpr int kShard = 3;   // one shard of a multi-GPU solve: reduce, exchange the boundary
+                            // pair with every peer over peer memory, top solve, expand
 
 constexpr int kFastThreads = 256;
 constexpr int kGenericThreads = 256;
@@ -37,6 +39,24 @@ struct IfacePtrs {
     T* rhs;
 };
 
+// Peer mailboxes of the fused multi-GPU solve (k_final<kShard>). Each rank owns
+// one mailbox in its HBM, mapped into every peer (CUDA IPC over NVLink/NVSwitch).
+// Entry (slot, p) = rank p's boundary pair {sub0, sub1, diag0, diag1, sup0,
+// sup1, rhs0, rhs1} (FP64) + a 64-bit epoch flag, 128 B apart; the two slots
+// alternate by epoch parity, so a rank one solve ahead never overwrites a pair
+// a slower peer is still reading.
+constexpr int kMaxPeers = 64;
+constexpr int kMailboxEntryDoubles = 16;
+constexpr int kExchangeLevel = 0x7FFF;  // err-word level of a peer-exchange timeout
+struct ShardLink {
+    double* peers[kMaxPeers];   // every rank's mailbox, by rank (peers[rank] = own)
+    double* own;                // this rank's mailbox
+    unsigned long long* epoch;  // exchanges completed by this context
+    int nranks;
+    int rank;
+};
+inline size_t mailbox_bytes(int nranks) { return (size_t)2 * nranks * kMailboxEntryDoubles * sizeof(double); }
+
 cudaError_t init_kernel_attributes();
 cudaError_t launch_reset(unsigned long long* err, cudaStream_t st);
 bool fast_shape(int64_t m, int* L, int* G);
@@ -60,7 +80,8 @@ cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs
                            int level, cudaStream_t st);
 template <class T>
 cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const IfacePtrs<T>& out,
-                         const T* xi, T* x, unsigned long long* err, int level, cudaStream_t st);
+                         const T* xi, T* x, unsigned long long* err, int level, cudaStream_t st,
+                         const ShardLink* link = nullptr);
 template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st);

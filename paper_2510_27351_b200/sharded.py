@@ -7,10 +7,17 @@ Per rank:
      assemble_interface rows of partition.hpp:139-149 for one super-block):
         E1_p: a1*x_{s_p - 1} + b1*x_{s_p} + g1*x_{e_p} = d1
         E2_p: a2*x_{s_p} + b2*x_{e_p} + g2*x_{e_p + 1} = d2
-  2. one all-gather of 8 doubles per rank (NCCL over NVLink on B200; gloo in
-     the CPU tests) — the only exchange step of the method;
+  2. one all-gather of 8 doubles per rank — the only exchange step of the
+     method;
   3. ``finish``  — every rank solves the 2P-row top system redundantly
      (Thomas, tridiagonal.hpp:52-72) and runs Stage 3 of its local levels.
+Two transports for step 2:
+  * ``"p2p"`` (default on GPUs): fused. Steps 1-3 are ONE captured graph per
+    rank; the finishing kernel stores the shard's pair straight into every
+    peer's HBM mailbox (CUDA IPC over NVLink/NVSwitch), waits on the peers'
+    epoch flags and solves the top system itself (tp_shard_solve_f64_dev).
+  * ``"nccl"``: reduce graph -> torch.distributed.all_gather_into_tensor ->
+    finish graph (also the gloo path of the CPU tests).
 The policy (m per level, R) is the kNN prediction for the GLOBAL N, as the
 reference would choose for the whole system (recursion_sizes, policy.hpp:25-45).
 """
@@ -87,12 +94,89 @@ class DeviceBackend:
         _raise(lib.tp_check_device_error(self.ctx.handle, C.byref(err)), err)
 
 
-class ShardedSolver:
-    """solve_partition over a process group: each rank passes its local shard."""
+class PeerLink:
+    """Peer mailboxes of the fused path: allocate this rank's mailbox, exchange
+    CUDA IPC handles over the process group (all_gather_object), open every
+    peer's, attach, barrier."""
 
-    def __init__(self, backend=None, group=None):
+    def __init__(self, ctx, group=None):
+        import torch.distributed as dist
+
+        self.ctx = ctx
+        P = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        own = C.c_void_p()
+        _call(lib.tp_shard_mailbox, ctx.handle, P, C.byref(own))
+        h = (C.c_uint8 * 64)()
+        _call(lib.tp_ipc_get_handle, ctx.handle, own, h)
+        allh = [None] * P
+        dist.all_gather_object(allh, bytes(h), group=group)
+        ptrs = (C.c_void_p * P)()
+        for p in range(P):
+            if p == rank:
+                ptrs[p] = own.value
+                continue
+            hp = (C.c_uint8 * 64).from_buffer_copy(allh[p])
+            dp = C.c_void_p()
+            _call(lib.tp_ipc_open_handle, ctx.handle, hp, C.byref(dp))
+            ptrs[p] = dp.value
+        _call(lib.tp_shard_attach, ctx.handle, P, rank, ptrs)
+        dist.barrier(group=group)  # every mailbox zeroed before anyone publishes
+        self.nranks, self.rank = P, rank
+
+
+def attach_local_peers(ctxs):
+    """Same-process peers (simulated ranks on one GPU): raw mailbox pointers."""
+    P = len(ctxs)
+    boxes = []
+    for c in ctxs:
+        own = C.c_void_p()
+        _call(lib.tp_shard_mailbox, c.handle, P, C.byref(own))
+        boxes.append(own.value)
+    ptrs = (C.c_void_p * P)(*boxes)
+    for r, c in enumerate(ctxs):
+        _call(lib.tp_shard_attach, c.handle, P, r, ptrs)
+
+
+def fused_solve(ctx, sys4, policy, out=None, stream=None, prepare_only: bool = False):
+    """tp_shard_solve_f64_dev on this rank's shard (device tensors);
+    prepare_only: capture + instantiate its graph without launching."""
+    import torch
+
+    sz = _policy_array(policy)
+    x = out if out is not None else torch.empty_like(sys4[1])
+    st = torch_stream() if stream is None else stream
+    fn = lib.tp_shard_prepare_f64_dev if prepare_only else lib.tp_shard_solve_f64_dev
+    _call(fn, ctx.handle, *[C.c_void_p(t.data_ptr()) for t in sys4],
+          int(sys4[0].numel()), sz.ctypes.data_as(C.POINTER(C.c_int64)), len(sz),
+          C.c_void_p(x.data_ptr()), C.c_void_p(st))
+    return x
+
+
+class ShardedSolver:
+    """solve_partition over a process group: each rank passes its local shard.
+
+    transport: "p2p" (fused peer-memory exchange inside the finishing kernel),
+    "nccl" (all-gather between two graphs) or "auto" (p2p, falling back to
+    nccl when the IPC link cannot be set up — e.g. non-CUDA backends)."""
+
+    def __init__(self, backend=None, group=None, transport: str = "nccl"):
         self.backend = backend or DeviceBackend()
         self.group = group
+        if transport not in ("p2p", "nccl", "auto"):
+            raise ValueError("transport must be 'p2p', 'nccl' or 'auto'")
+        self.transport = transport
+        self.link = None
+        self.fallback_reason = None
+        if transport in ("p2p", "auto"):
+            try:
+                self.link = PeerLink(self.backend.ctx, group)
+                self.transport = "p2p"
+            except Exception as e:  # noqa: BLE001 - reported, then NCCL
+                if transport == "p2p":
+                    raise
+                self.fallback_reason = f"{type(e).__name__}: {e}"
+                self.transport = "nccl"
 
     def policy_for(self, n_global: int, policy=None) -> RecursionPolicy:
         if policy is None:
@@ -103,6 +187,10 @@ class ShardedSolver:
         import torch.distributed as dist
 
         pol = self.policy_for(n_global, policy)
+        if self.transport == "p2p":
+            x = fused_solve(self.backend.ctx, sys4, pol, out=out)
+            self.backend.launches = self.backend.ctx.last_launch_count()
+            return x
         P = dist.get_world_size(self.group)
         rank = dist.get_rank(self.group)
         eq8 = self.backend.reduce(sys4, pol)
@@ -140,3 +228,50 @@ def simulate_ranks(sub, diag, sup, rhs, nranks: int, policy=None) -> np.ndarray:
     for be in ctxs:
         be.ctx.close()
     return x
+
+
+def simulate_ranks_fused(sub, diag, sup, rhs, nranks: int, policy=None, repeats: int = 1):
+    """The fused peer-memory path with `nranks` simulated ranks on ONE GPU:
+    one context (own stream) per rank, mailboxes linked by raw pointers, all
+    ranks' graphs in flight at once (their finishing kernels wait on each
+    other's epoch flags). Every rank's kernels must be able to start while a
+    peer's finishing kernel waits, so all graphs are instantiated first and the
+    process should be started with CUDA_MODULE_LOADING=EAGER (a lazily loaded
+    kernel waits for the device to go idle) and CUDA_DEVICE_MAX_CONNECTIONS=32
+    (a hardware queue per stream)."""
+    import torch
+
+    from ._lib import TpError
+    from .tridpart import Context
+
+    n = len(diag)
+    pol = RecursionPolicy(policy) if policy is not None else predicted_policy(n)
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (sub, diag, sup, rhs)]
+    ctxs = [Context(torch.cuda.current_device()) for _ in range(nranks)]
+    attach_local_peers(ctxs)
+    shards = []
+    for r in range(nranks):
+        lo, cnt = shard_bounds(n, nranks, r)
+        sys4 = [torch.from_numpy(a[lo:lo + cnt].copy()).cuda() for a in arrs]
+        # size each context's workspace up front (same plan as the fused solve)
+        # so no allocation happens while other ranks' kernels wait on flags
+        DeviceBackend(ctxs[r]).reduce(sys4, pol)
+        shards.append((lo, cnt, sys4, torch.empty(cnt, dtype=torch.float64, device="cuda")))
+    # every graph instantiated before any rank's exchange is in flight
+    for r, (lo, cnt, sys4, xr) in enumerate(shards):
+        fused_solve(ctxs[r], sys4, pol, out=xr, stream=0, prepare_only=True)
+    torch.cuda.synchronize()
+    xs = []
+    for _ in range(repeats):
+        for r, (lo, cnt, sys4, xr) in enumerate(shards):
+            fused_solve(ctxs[r], sys4, pol, out=xr, stream=0)  # NULL -> the context's own stream
+        torch.cuda.synchronize()
+        x = np.empty(n)
+        for r, (lo, cnt, sys4, xr) in enumerate(shards):
+            err = TpError()
+            _raise(lib.tp_check_device_error(ctxs[r].handle, C.byref(err)), err)
+            x[lo:lo + cnt] = xr.cpu().numpy()
+        xs.append(x)
+    for c in ctxs:
+        c.close()
+    return xs[0] if repeats == 1 else xs
