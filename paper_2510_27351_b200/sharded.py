@@ -106,21 +106,38 @@ class PeerLink:
         P = dist.get_world_size(group)
         rank = dist.get_rank(group)
         own = C.c_void_p()
-        _call(lib.tp_shard_mailbox, ctx.handle, P, C.byref(own))
-        h = (C.c_uint8 * 64)()
-        _call(lib.tp_ipc_get_handle, ctx.handle, own, h)
+        why, hb = None, b""
+        try:
+            _call(lib.tp_shard_mailbox, ctx.handle, P, C.byref(own))
+            h = (C.c_uint8 * 64)()
+            _call(lib.tp_ipc_get_handle, ctx.handle, own, h)
+            hb = bytes(h)
+        except Exception as e:  # noqa: BLE001 - decided collectively below
+            why = f"rank {rank}: {type(e).__name__}: {e}"
         allh = [None] * P
-        dist.all_gather_object(allh, bytes(h), group=group)
+        dist.all_gather_object(allh, hb, group=group)
         ptrs = (C.c_void_p * P)()
-        for p in range(P):
-            if p == rank:
-                ptrs[p] = own.value
-                continue
-            hp = (C.c_uint8 * 64).from_buffer_copy(allh[p])
-            dp = C.c_void_p()
-            _call(lib.tp_ipc_open_handle, ctx.handle, hp, C.byref(dp))
-            ptrs[p] = dp.value
-        _call(lib.tp_shard_attach, ctx.handle, P, rank, ptrs)
+        try:
+            if why is not None or any(len(x) != 64 for x in allh):
+                raise RuntimeError("a rank has no mailbox handle")
+            for p in range(P):
+                if p == rank:
+                    ptrs[p] = own.value
+                    continue
+                hp = (C.c_uint8 * 64).from_buffer_copy(allh[p])
+                dp = C.c_void_p()
+                _call(lib.tp_ipc_open_handle, ctx.handle, hp, C.byref(dp))
+                ptrs[p] = dp.value
+            _call(lib.tp_shard_attach, ctx.handle, P, rank, ptrs)
+        except Exception as e:  # noqa: BLE001 - decided collectively below
+            why = why or f"rank {rank}: {type(e).__name__}: {e}"
+        # every rank takes the same transport: a rank left on p2p while a peer
+        # fell back to NCCL would wait for flags that never come
+        verdicts = [None] * P
+        dist.all_gather_object(verdicts, why, group=group)
+        failed = [v for v in verdicts if v is not None]
+        if failed:
+            raise RuntimeError("peer links unavailable: " + "; ".join(failed))
         dist.barrier(group=group)  # every mailbox zeroed before anyone publishes
         self.nranks, self.rank = P, rank
 

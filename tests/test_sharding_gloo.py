@@ -16,11 +16,16 @@ import torch.multiprocessing as mp
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+class _NoDevice:
+    handle = None  # a NULL tp_ctx*: the C-ABI answers TP_ERR_INVALID_ARGUMENT
+
+
 class OracleBackend:
     """reduce/finish on the CPU with the oracle (test scaffold, not a product path)."""
 
     def __init__(self, oracle):
         self.o = oracle
+        self.ctx = _NoDevice()  # peer links need a device context: p2p is refused
 
     def reduce(self, sys4, policy):
         s = self.o.System(*(t.numpy() for t in sys4))
@@ -55,7 +60,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, seed, q):
+def _worker(rank, world, port, n, seed, q, transport="nccl"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -68,21 +73,24 @@ def _worker(rank, world, port, n, seed, q):
         glob = oracle.generate_system(n, seed)
         lo, cnt = shard_bounds(n, world, rank)
         sys4 = [torch.from_numpy(a[lo:lo + cnt].copy()) for a in (glob.sub, glob.diag, glob.sup, glob.rhs)]
-        solver = ShardedSolver(backend=OracleBackend(oracle))
+        solver = ShardedSolver(backend=OracleBackend(oracle), transport=transport)
         pol = solver.policy_for(n)
         x = solver.solve(sys4, n)
-        q.put((rank, lo, x.numpy(), pol.sizes))
+        q.put((rank, lo, x.numpy(), pol.sizes, solver.transport, solver.fallback_reason))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_solve_gloo(oracle_mod, world):
+@pytest.mark.parametrize("world,transport", [(2, "nccl"), (3, "nccl"), (2, "auto")])
+def test_sharded_solve_gloo(oracle_mod, world, transport):
+    """transport="auto" on CPU: no rank can build peer links, every rank sees
+    the same collective verdict and all fall back to the all-gather together
+    (a split decision would leave ranks waiting on each other forever)."""
     n, seed = 100_003, 31
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, seed, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, seed, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
@@ -92,8 +100,11 @@ def test_sharded_solve_gloo(oracle_mod, world):
     glob = oracle_mod.generate_system(n, seed)
     ref = oracle_mod.solve_partition(glob, [32])
     x = np.empty(n)
-    for rank, lo, xr, sizes in res:
+    for rank, lo, xr, sizes, used, why in res:
         assert sizes == [32]  # kNN policy of the GLOBAL N (predict(1e5) = 32, R = 0)
+        assert used == "nccl"
+        if transport == "auto":
+            assert why is not None and all(f"rank {r}" in why for r in range(world))
         x[lo:lo + len(xr)] = xr
     assert oracle_mod.rel_inf_diff(x, ref) <= 1e-10
     assert oracle_mod.residual_inf(glob, x) <= 1e-12
