@@ -14,6 +14,8 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
+
 #include "tp_device.cuh"
 #include "tp_kernels.h"
 #include "tp_fast.cuh"
@@ -528,6 +530,228 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
 }
 
 // ===========================================================================
+// Finishing solve on a thread-block CLUSTER (kFinCS CTAs on kFinCS SMs, DSMEM).
+// The single-CTA k_final is FP64-latency and shared-memory-bandwidth bound
+// (~10 rows per thread swept from smem, a 9-level tree, ~21K cycles at C3).
+// Here Gtot = min(kFinCS * kFinNT, pow2floor(n/2)) chunks of <= 4 rows each
+// live in registers; the tree is 5 shuffle levels per warp, <= 3 levels over
+// the warp roots of each CTA (warp 0), and <= 3 levels over the CTA roots in
+// CTA 0, which reads them from the peers' shared memory (cluster.map_shared_rank),
+// handles the root (kSolve / kStage1 / kStage3 / kShard exactly as k_final),
+// and writes each CTA's segment ends back into that CTA's shared memory. Two
+// cluster barriers in total. Same merges / sweeps / expansion as k_final, so
+// results agree with it to rounding.
+// ===========================================================================
+constexpr int kFinCS = 8;     // CTAs per cluster (portable maximum)
+constexpr int kFinNT = 256;   // threads per CTA
+constexpr int kFinRows = kFinNT * 4;  // rows staged per CTA (chunks <= 4 rows)
+
+template <class T, int MODE>
+__global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
+    k_final_cl(SysPtrs<T> sys, int64_t n, int gtot, IfacePtrs<T> out, const T* __restrict__ xi,
+               T* __restrict__ x, unsigned long long* err, int level, const __grid_constant__ ShardLink link) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ T sa[kFinRows], sb[kFinRows], sc[kFinRows], sd[kFinRows];
+    __shared__ Eq2<T> wroot[kFinNT / 32];
+    __shared__ Eq2<T> croot;   // this CTA's root pair, read by CTA 0
+    __shared__ T cx[2];        // this CTA's (x_s, x_e), written by CTA 0
+    __shared__ T wx[2 * (kFinNT / 32)];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int cta = (int)cl.block_rank();
+    RowGuard bad;
+    pdl_begin();
+
+    const int per = gtot / kFinCS;  // chunks owned by this CTA (power of two)
+    const int64_t Llo = n / gtot, ext = n % gtot;
+    auto cstart = [&](int64_t g) { return g * Llo + (g < ext ? g : ext); };
+    const int64_t g0 = (int64_t)cta * per;
+    const int64_t r0 = cstart(g0);
+    const int rows = (int)(cstart(g0 + per) - r0);
+    for (int i = tid; i < rows; i += kFinNT) {
+        sa[i] = __ldg(sys.sub + r0 + i);
+        sb[i] = __ldg(sys.diag + r0 + i);
+        sc[i] = __ldg(sys.sup + r0 + i);
+        sd[i] = __ldg(sys.rhs + r0 + i);
+    }
+    __syncthreads();
+
+    // ---- leaf: this thread's chunk (2..4 rows) in registers ----
+    const bool active = tid < per;
+    const int64_t g = g0 + tid;
+    const int len = active ? (int)(Llo + (g < ext ? 1 : 0)) : 2;
+    const int64_t grow = active ? cstart(g) : 0;
+    Chunk<T, 4> r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const bool live = active && i < len;
+        const int li = (int)(grow - r0) + i;
+        r.a[i] = live ? sa[li] : T(0);
+        r.b[i] = live ? sb[li] : T(1);
+        r.c[i] = live ? sc[li] : T(0);
+        r.d[i] = live ? sd[li] : T(0);
+    }
+    T rb[4], gm[4], dl[4];
+    Eq2<T> cur;
+    if (len == 2) cur = leaf_reduce_keep<T, 4, 2>(r, grow, bad, rb, gm, dl);
+    else if (len == 3) cur = leaf_reduce_keep<T, 4, 3>(r, grow, bad, rb, gm, dl);
+    else cur = leaf_reduce_keep<T, 4, 4>(r, grow, bad, rb, gm, dl);
+    if (!active) cur = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
+
+    // ---- warp levels (chunk index inside the CTA == tid) ----
+    MergeSave<T> sw[5];
+#pragma unroll
+    for (int lv = 0; lv < 5; ++lv) {
+        const int h = 1 << lv;
+        const Eq2<T> oth = shfl_down_eq(cur, h);
+        if (h < per && (lane & (2 * h - 1)) == 0 && tid + h < per)
+            cur = merge(cur, oth, cstart(g + h) - 1, bad, sw[lv]);
+    }
+    const int nwr = per >= 32 ? per / 32 : 1;
+    if (lane == 0 && warp < nwr) wroot[warp] = cur;
+    __syncthreads();
+
+    // ---- warp 0: the CTA's warp roots (<= 3 levels) ----
+    MergeSave<T> sx[3];
+    Eq2<T> wc = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
+    if (warp == 0) {
+        wc = lane < nwr ? wroot[lane] : wc;
+#pragma unroll
+        for (int lv = 0; lv < 3; ++lv) {
+            const int h = 1 << lv;
+            const Eq2<T> oth = shfl_down_eq(wc, h);
+            if (h < nwr && (lane & (2 * h - 1)) == 0 && lane + h < nwr)
+                wc = merge(wc, oth, cstart(g0 + 32 * (lane + h)) - 1, bad, sx[lv]);
+        }
+        if (lane == 0) croot = wc;
+    }
+    cl.sync();
+
+    // ---- CTA 0, warp 0: the CTA roots (3 levels), the root, and back down ----
+    if (cta == 0 && warp == 0) {
+        Eq2<T> cc = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
+        if (lane < kFinCS) cc = *cl.map_shared_rank(&croot, lane);
+        MergeSave<T> sc3[3];
+#pragma unroll
+        for (int lv = 0; lv < 3; ++lv) {
+            const int h = 1 << lv;
+            const Eq2<T> oth = shfl_down_eq(cc, h);
+            if ((lane & (2 * h - 1)) == 0 && lane + h < kFinCS)
+                cc = merge(cc, oth, cstart((int64_t)per * (lane + h)) - 1, bad, sc3[lv]);
+        }
+        T xs = 0, xe = 0;
+        if (lane == 0) {
+            if constexpr (MODE == kStage1) {
+                out.sub[0] = cc.a1;  out.sub[1] = cc.a2;
+                out.diag[0] = cc.b1; out.diag[1] = cc.b2;
+                out.sup[0] = cc.g1;  out.sup[1] = cc.g2;
+                out.rhs[0] = cc.d1;  out.rhs[1] = cc.d2;
+            } else if constexpr (MODE == kStage3) {
+                xs = xi[0];
+                xe = xi[1];
+            } else if constexpr (MODE == kShard) {
+                __shared__ double top_cm[2 * kMaxPeers], top_x[2 * kMaxPeers];
+                RowGuard top_bad;
+                int missing = -1;
+                if (!shard_exchange(link, cc, top_cm, top_x, xs, xe, top_bad, missing)) {
+                    if (err != nullptr)
+                        atomicMin(err, ((unsigned long long)kExchangeLevel << 48) | (unsigned long long)missing);
+                }
+                report_pivot(err, level + 1, top_bad.bad);
+            } else {
+                root_solve(cc, n - 1, bad, xs, xe);
+            }
+        }
+        if constexpr (MODE != kStage1) {
+#pragma unroll
+            for (int lv = 2; lv >= 0; --lv) {
+                const int h = 1 << lv;
+                T xt = 0;
+                if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sc3[lv], xs, xe);
+                const T rxt = __shfl_up_sync(0xffffffffu, xt, h);
+                const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
+                if ((lane & (2 * h - 1)) == h) {
+                    xs = first_from_e1(cc, rxt, rxe);
+                    xe = rxe;
+                } else if ((lane & (2 * h - 1)) == 0) {
+                    xe = xt;
+                }
+            }
+            if (lane < kFinCS) {
+                T* dst = cl.map_shared_rank(&cx[0], lane);
+                dst[0] = xs;
+                dst[1] = xe;
+            }
+        }
+    }
+    if constexpr (MODE == kStage1) {
+        // CTA 0 read every croot before reaching this barrier; no CTA may exit
+        // while its shared memory can still be read
+        cl.sync();
+        report_pivot(err, level, bad.bad);
+        return;
+    }
+    cl.sync();
+
+    // ---- warp 0 of every CTA: down its warp-root levels ----
+    if (warp == 0) {
+        T xs = lane == 0 ? cx[0] : T(0), xe = lane == 0 ? cx[1] : T(0);
+#pragma unroll
+        for (int lv = 2; lv >= 0; --lv) {
+            const int h = 1 << lv;
+            if (h >= nwr) continue;
+            T xt = 0;
+            if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sx[lv], xs, xe);
+            const T rxt = __shfl_up_sync(0xffffffffu, xt, h);
+            const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
+            if ((lane & (2 * h - 1)) == h) {
+                xs = first_from_e1(wc, rxt, rxe);
+                xe = rxe;
+            } else if ((lane & (2 * h - 1)) == 0) {
+                xe = xt;
+            }
+        }
+        if (lane < nwr) {
+            wx[2 * lane] = xs;
+            wx[2 * lane + 1] = xe;
+        }
+    }
+    __syncthreads();
+
+    // ---- every warp: its warp levels, then the chunk ----
+    T xs = 0, xe = 0;
+    if (lane == 0 && warp < nwr) {
+        xs = wx[2 * warp];
+        xe = wx[2 * warp + 1];
+    }
+#pragma unroll
+    for (int lv = 4; lv >= 0; --lv) {
+        const int h = 1 << lv;
+        if (h >= per) continue;
+        T xt = 0;
+        if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sw[lv], xs, xe);
+        const T rxt = __shfl_up_sync(0xffffffffu, xt, h);
+        const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
+        if ((lane & (2 * h - 1)) == h) {
+            xs = first_from_e1(cur, rxt, rxe);
+            xe = rxe;
+        } else if ((lane & (2 * h - 1)) == 0) {
+            xe = xt;
+        }
+    }
+    if (active) {
+        T xv[4];
+        if (len == 2) leaf_expand<T, 4, 2>(r, rb, gm, dl, xs, xe, xv);
+        else if (len == 3) leaf_expand<T, 4, 3>(r, rb, gm, dl, xs, xe, xv);
+        else leaf_expand<T, 4, 4>(r, rb, gm, dl, xs, xe, xv);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (i < len) x[grow + i] = xv[i];
+    }
+    report_pivot(err, level, bad.bad);
+}
+
+// ===========================================================================
 // Sharded top level: every rank holds the gathered [eq8 x P] (layout per rank:
 // sub[2], diag[2], sup[2], rhs[2]); assemble the 2P-row interface
 // (assemble_interface, partition.hpp:139-149) and solve it with Thomas
@@ -817,6 +1041,11 @@ cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs
                     out, xi, x, err, level);
 }
 
+// The cluster finishing solve (k_final_cl) takes every system of at least
+// kFinClusterMin rows (TPB_FINAL_CLUSTER=0 keeps the single-CTA k_final).
+constexpr int64_t kFinClusterMin = 64;
+static bool g_final_cluster = true;
+
 static int final_G(int64_t n) {
     int G = 1;
     while (G * 2 <= kFinalThreads2 && n / (G * 2) >= 2) G *= 2;
@@ -830,6 +1059,17 @@ cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const Iface
     if (n > kFinalCap || n < 1) return cudaErrorInvalidValue;
     if (mode == kShard && (link == nullptr || link->nranks < 1 || link->nranks > kMaxPeers))
         return cudaErrorInvalidValue;
+    if (g_final_cluster && n >= kFinClusterMin) {
+        int gtot = kFinCS;
+        while (gtot * 2 <= kFinCS * kFinNT && n / (gtot * 2) >= 2) gtot *= 2;
+        auto kc = mode == kStage1   ? k_final_cl<T, kStage1>
+                  : mode == kStage3 ? k_final_cl<T, kStage3>
+                  : mode == kShard  ? k_final_cl<T, kShard>
+                                    : k_final_cl<T, kSolve>;
+        const ShardLink none{};
+        return launch_k(kc, kFinCS, kFinNT, 0, st, sys, n, gtot, out, xi, x, err, level,
+                        link != nullptr ? *link : none);
+    }
     const int G = final_G(n);
     const size_t smem = (size_t)(4 * n) * sizeof(T);
     auto k = mode == kStage1   ? k_final<T, kStage1>
@@ -871,6 +1111,7 @@ static cudaError_t set_carveout(int pct) {
 
 cudaError_t init_kernel_attributes() {
     if (const char* v = getenv("TPB_PDL")) g_pdl = atoi(v) != 0;
+    if (const char* v = getenv("TPB_FINAL_CLUSTER")) g_final_cluster = atoi(v) != 0;
     cudaError_t e = set_smem_attributes<double>();
     if (e == cudaSuccess) e = set_smem_attributes<float>();
     if (const char* v = getenv("TPB_CARVEOUT")) {

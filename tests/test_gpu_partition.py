@@ -348,3 +348,30 @@ def test_async_host_solves_on_two_contexts(tp, oracle_mod):
         _check(oracle_mod, s, out.numpy(), ref)
     for c in ctxs:
         c.close()
+
+
+def test_single_cta_finishing_solve_still_matches(tp):
+    """TPB_FINAL_CLUSTER=0 keeps the single-CTA k_final (the default is the
+    8-CTA cluster kernel for systems >= 64 rows); both must pass parity."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import json, sys
+sys.path.insert(0, {root!r})
+import oracle, paper_2510_27351_b200 as tp
+out = []
+for n, sizes in ((10_000, [4]), (1_000_000, [32]), (300_001, [16, 8]), (6_000, [3000])):
+    s = oracle.generate_system(n, 7)
+    ref = oracle.solve_partition(s, sizes)
+    x = tp.solve_partition(tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs), tp.RecursionPolicy(sizes))
+    out.append([oracle.rel_inf_diff(x, ref), oracle.floored_rel_diff(x, ref), oracle.residual_inf(s, x)])
+print(json.dumps(out))
+"""
+    env = dict(os.environ, TPB_FINAL_CLUSTER="0")
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    for d, f, r in json.loads(res.stdout.strip().splitlines()[-1]):
+        assert d <= TOL_NORM and f <= TOL_FLOOR and r <= TOL_RES
