@@ -375,3 +375,18 @@ print(json.dumps(out))
     assert res.returncode == 0, res.stderr[-2000:]
     for d, f, r in json.loads(res.stdout.strip().splitlines()[-1]):
         assert d <= TOL_NORM and f <= TOL_FLOOR and r <= TOL_RES
+
+
+@pytest.mark.parametrize("n", [40, 100, 1000, 6000])
+def test_zero_pivot_in_the_finishing_solve(tp, n):
+    """thomas_solve runs the finishing solve directly (single CTA below 64
+    rows, the 8-CTA cluster kernel above): a zero row anywhere must surface
+    as ZeroPivotError, and a clean system of the same size must solve."""
+    sub, diag, sup, rhs = np.zeros(n), np.ones(n), np.zeros(n), np.ones(n)
+    x = tp.thomas_solve(tp.TridiagonalSystem(sub, diag, sup, rhs))
+    assert np.allclose(x, 1.0)
+    for row in (0, n // 2, n - 1):
+        d = diag.copy()
+        d[row] = 0.0
+        with pytest.raises(tp.ZeroPivotError):
+            tp.thomas_solve(tp.TridiagonalSystem(sub, d, sup, rhs))
