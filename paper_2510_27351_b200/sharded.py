@@ -185,6 +185,7 @@ class ShardedSolver:
         self.transport = transport
         self.link = None
         self.fallback_reason = None
+        self._verified = False
         if transport in ("p2p", "auto"):
             try:
                 self.link = PeerLink(self.backend.ctx, group)
@@ -194,6 +195,33 @@ class ShardedSolver:
                     raise
                 self.fallback_reason = f"{type(e).__name__}: {e}"
                 self.transport = "nccl"
+
+    def _verify_first(self, sys4, n_global, pol, x, out):
+        """After the first fused solve every rank checks that its peer
+        exchange completed; if any rank timed out (peer writes not arriving),
+        all ranks switch to the all-gather transport together and redo it."""
+        import torch
+        import torch.distributed as dist
+
+        from ._lib import NCCL, TpError
+
+        torch.cuda.synchronize()
+        err = TpError()
+        st = lib.tp_check_device_error(self.backend.ctx.handle, C.byref(err))
+        mine = None
+        if st == NCCL:
+            mine = f"rank {dist.get_rank(self.group)}: {err.msg.decode(errors='replace')}"
+        elif st != 0:
+            _raise(st, err)  # a genuine solver error (zero pivot, ...)
+        verdicts = [None] * dist.get_world_size(self.group)
+        dist.all_gather_object(verdicts, mine, group=self.group)
+        self._verified = True
+        failed = [v for v in verdicts if v is not None]
+        if not failed:
+            return x
+        self.transport = "nccl"
+        self.fallback_reason = "peer exchange failed on the first solve: " + "; ".join(failed)
+        return self.solve(sys4, n_global, pol, out=out)
 
     def policy_for(self, n_global: int, policy=None) -> RecursionPolicy:
         if policy is None:
@@ -207,6 +235,8 @@ class ShardedSolver:
         if self.transport == "p2p":
             x = fused_solve(self.backend.ctx, sys4, pol, out=out)
             self.backend.launches = self.backend.ctx.last_launch_count()
+            if not self._verified:
+                x = self._verify_first(sys4, n_global, pol, x, out)
             return x
         P = dist.get_world_size(self.group)
         rank = dist.get_rank(self.group)
