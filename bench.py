@@ -39,7 +39,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--n", type=float, default=1e8, help="unknowns per GPU")
+    p.add_argument("--n", "--size", dest="n", type=float, default=1e8,
+                   help="unknowns per GPU (--size under torchrun: its own --n* options shadow --n)")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=6)
@@ -67,6 +68,10 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("TPB_SHARE_GPU") == "1":
+        # functional check of the multi-rank flow on a 1-GPU box: every rank on
+        # device 0 (timings are meaningless: the processes time-slice the GPU)
+        local = 0
     return world, rank, local
 
 
@@ -221,7 +226,10 @@ def run_ours(args):
         if "RANK" not in os.environ:  # --force-sharded without torchrun: a 1-rank group
             os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
                               MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("TPB_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")  # NCCL refuses two ranks on one GPU
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_per = int(args.n)
     n_glob = n_per * world
     policy = tp.predicted_policy(n_glob)
@@ -267,12 +275,11 @@ def run_ours(args):
         barrier()
     ms = ev0.elapsed_time(ev1)
     launches_per_step = solver.backend.launches if sharded_mode else ctx.last_launch_count()
+    red_dev = "cpu" if os.environ.get("TPB_SHARE_GPU") == "1" else "cuda"  # gloo reduces host tensors
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        if world > 1:
-            launches_per_step += 0  # the all-gather is NCCL's, not counted as ours
     ms_step = ms / args.steps
     value = n_glob * args.steps / (ms / 1e3)
 
@@ -280,8 +287,13 @@ def run_ours(args):
     tp.check_device_error()
     res = tp.residual_inf(sys_d, x) if world == 1 else None
     if world > 1:
-        # residual of the local rows (shard-boundary rows need neighbours; skip them)
-        res = tp.residual_inf(tp.TridiagonalSystem(*(t[1:-1] for t in sys4)), x[1:-1]) if n_loc > 2 else 0.0
+        # residual_inf over this shard's rows 1..n_loc-2 (their neighbours are
+        # local; the two boundary rows couple to the adjacent shards), max over ranks
+        a_, b_, c_, d_ = sys4
+        r_ = b_[1:-1] * x[1:-1] + a_[1:-1] * x[:-2] + c_[1:-1] * x[2:] - d_[1:-1]
+        num_d = torch.stack([r_.abs().max(), d_.abs().max()]).cpu()
+        dist.all_reduce(num_d, op=dist.ReduceOp.MAX)
+        res = float(num_d[0]) / max(1.0, float(num_d[1]))
 
     # per-kernel durations (CUDA events on the launch stream, same inputs)
     prof = {}
@@ -362,7 +374,7 @@ def run_ours(args):
         barrier()
         dt = time.perf_counter() - t0
         if dist is not None:
-            t = torch.tensor([dt], device="cuda")
+            t = torch.tensor([dt], device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": n_glob * args.e2e_steps / dt, "unit": UNIT,

@@ -198,3 +198,28 @@ def test_fused_two_processes_cuda_ipc(tp, oracle_mod):
         x[lo:lo + len(xr)] = xr
         assert repeat_equal
     _check(oracle_mod, s, x, ref)
+
+
+@pytest.mark.parametrize("world,transport", [(2, "auto"), (3, "nccl")])
+def test_bench_multi_rank_flow_on_one_gpu(world, transport):
+    """bench.py's N>1 path (torchrun, one process per rank, sharded solve,
+    max-over-ranks timing, one JSON line from rank 0) with every rank on the
+    one GPU of this box (TPB_SHARE_GPU=1: gloo process group, the ranks
+    time-slice the GPU, so only correctness and the output contract are
+    checked)."""
+    import json
+    import subprocess
+
+    env = dict(os.environ, TPB_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", str(world), "--steps", "3", "--warmup", "3", "--prewarm", "0", "--e2e-steps", "1",
+           "--size", "4e6", "--transport", transport]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world and d["config"]["n_global"] == 4_000_000 * world
+    assert d["config"]["transport"] == ("p2p" if transport == "auto" else "nccl")
+    assert d["residual"] <= 1e-12 and d["value"] > 0 and d["gpu_launches"] > 0
