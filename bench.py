@@ -258,9 +258,15 @@ def run_ours(args):
     # untimed: graph capture + clock ramp (~0.3 s of solves), then W warm-up steps
     step()
     barrier()
-    t_end = time.perf_counter() + args.prewarm
-    while time.perf_counter() < t_end:
-        step()
+    if not sharded_mode:
+        t_end = time.perf_counter() + args.prewarm
+        while time.perf_counter() < t_end:
+            step()
+    else:
+        # every rank must issue the same number of solves (each one pairs with the
+        # peers' solve of the same index), so the ramp is a count, not a deadline
+        for _ in range(int(args.prewarm * 800)):
+            step()
     for _ in range(args.warmup):
         step()
     barrier()
