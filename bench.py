@@ -165,7 +165,8 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    n = int(args.n)
+    n_arm = int(args.n) * max(1, args.gpus)  # our arm's global N at this GPU count
+    n = n_arm
     # bound the run: ~3 s per N=1e8 solve on 16 cores; keep the whole run ~<= 3 min
     budget_s = 150.0
     per = 3.5 * n / 1e8
@@ -191,7 +192,8 @@ def run_reference(args):
         lib.ref_system_free(h)
     value = n * args.steps / dt
     cores = int(lib.ref_hardware_concurrency())
-    sample = (f"N={n} per step (generate_system seed={args.seed}), reference policy "
+    sample = (f"N={n} per step (generate_system seed={args.seed}; our arm's global N is {n_arm}, "
+              f"bounded to ~{budget_s:.0f} s of CPU work), reference policy "
               f"{[int(v) for v in sizes]}, {args.warmup} warm-up + {args.steps} timed solves")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
