@@ -560,7 +560,9 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int cta = (int)cl.block_rank();
     RowGuard bad;
+    TP_TRACE_DECL;
     pdl_begin();
+    TP_TRACE(0);
 
     const int per = gtot / kFinCS;  // chunks owned by this CTA (power of two)
     const int64_t Llo = n / gtot, ext = n % gtot;
@@ -575,6 +577,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         sd[i] = __ldg(sys.rhs + r0 + i);
     }
     __syncthreads();
+    TP_TRACE(1);
 
     // ---- leaf: this thread's chunk (2..4 rows) in registers ----
     const bool active = tid < per;
@@ -597,6 +600,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
     else if (len == 3) cur = leaf_reduce_keep<T, 4, 3>(r, grow, bad, rb, gm, dl);
     else cur = leaf_reduce_keep<T, 4, 4>(r, grow, bad, rb, gm, dl);
     if (!active) cur = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
+    TP_TRACE(2);
 
     // ---- warp levels (chunk index inside the CTA == tid) ----
     MergeSave<T> sw[5];
@@ -610,6 +614,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
     const int nwr = per >= 32 ? per / 32 : 1;
     if (lane == 0 && warp < nwr) wroot[warp] = cur;
     __syncthreads();
+    TP_TRACE(3);
 
     // ---- warp 0: the CTA's warp roots (<= 3 levels) ----
     MergeSave<T> sx[3];
@@ -625,7 +630,9 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         }
         if (lane == 0) croot = wc;
     }
+    TP_TRACE(4);
     cl.sync();
+    TP_TRACE(5);
 
     // ---- CTA 0, warp 0: the CTA roots (3 levels), the root, and back down ----
     if (cta == 0 && warp == 0) {
@@ -684,6 +691,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
             }
         }
     }
+    TP_TRACE(6);
     if constexpr (MODE == kStage1) {
         // CTA 0 read every croot before reaching this barrier; no CTA may exit
         // while its shared memory can still be read
@@ -692,6 +700,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         return;
     }
     cl.sync();
+    TP_TRACE(7);
 
     // ---- warp 0 of every CTA: down its warp-root levels ----
     if (warp == 0) {
@@ -717,6 +726,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         }
     }
     __syncthreads();
+    TP_TRACE(8);
 
     // ---- every warp: its warp levels, then the chunk ----
     T xs = 0, xe = 0;
@@ -748,6 +758,10 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         for (int i = 0; i < 4; ++i)
             if (i < len) x[grow + i] = xv[i];
     }
+    TP_TRACE(9);
+    TP_TRACE(10);
+    TP_TRACE(11);
+    if (blockIdx.x == 0) TP_TRACE_FLUSH;
     report_pivot(err, level, bad.bad);
 }
 

@@ -14,7 +14,10 @@ for n, pol in ((int(1e8), [64, 10, 32, 16]), (int(1e6), [32]), (int(1e9), [64, 1
     tr = (C.c_uint64 * 16)()
     _lib.lib.tp_debug_trace(tr)
     t = np.array(tr[:12], dtype=np.int64)
-    names = ["load", "leaf", "warptree", "sync1", "w0 merge", "w0 root+down", "sync2", "warp down", "leaf back", "sync3", "store"]
+    cl = os.environ.get("TPB_FINAL_CLUSTER", "1") != "0"
+    names = (["stage", "leaf", "warp tree+sync", "w0 merges", "cluster sync1", "cta0 root work", "cluster sync2",
+              "w0 down+sync", "warp down+expand+store", "-", "-"] if cl else
+             ["load", "leaf", "warptree", "sync1", "w0 merge", "w0 root+down", "sync2", "warp down", "leaf back", "sync3", "store"])
     print(n, pol, tp.plan_levels(n, pol)[2], "total cycles", t[11] - t[0])
     for i, nm in enumerate(names):
         print(f"   {nm:14s} {t[i+1]-t[i]:7d}")
