@@ -204,7 +204,6 @@ struct tp_ctx {
     void* dsys = nullptr;                 // host-path staging (5 arrays)
     size_t dsys_cap = 0;                  // bytes
     int64_t last_launches = 0;
-    std::vector<std::pair<int64_t, int>> occ;  // (key, grid cap)
     struct GraphEntry {
         std::vector<int64_t> key;
         cudaGraphExec_t exec = nullptr;
@@ -217,17 +216,6 @@ struct tp_ctx {
 
 namespace {
 
-template <class T>
-int fast_grid_cap(tp_ctx* ctx, int64_t m, bool vec, int mode) {
-    const int64_t key = (m << 4) | ((int64_t)sizeof(T) << 2) | (vec ? 2 : 0) | mode;
-    for (auto& kv : ctx->occ)
-        if (kv.first == key) return kv.second;
-    int nb = tpb::fast_max_active_blocks<T>(m, vec, mode);
-    if (nb < 1) nb = 1;
-    const int cap = nb * ctx->sms;
-    ctx->occ.push_back({key, cap});
-    return cap;
-}
 
 using KernelHook = void (*)(void* user, const char* name);
 
@@ -259,7 +247,7 @@ struct Runner {
             const bool vec = aligned32(L.in.sub) && aligned32(L.in.diag) && aligned32(L.in.sup) &&
                              aligned32(L.in.rhs) && (s1 || aligned32(L.x_out));
             check(tpb::launch_fast<T>(L.m, vec, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
-                                      ctx->d_err, level, fast_grid_cap<T>(ctx, L.m, vec, mode), st));
+                                      ctx->d_err, level, st));
             after(s1 ? "stage1" : "stage3", level);
         } else if (tpb::fast_rt_G(L.m) > 0) {
             check(tpb::launch_fast_rt<T>(L.m, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,

@@ -904,9 +904,11 @@ cudaError_t launch_reset(unsigned long long* err, cudaStream_t st) {
     return launch_k(k_reset, 1, 32, 0, st, err);
 }
 
-// Launch shapes chosen by measurement (scratch/tune.cu on B200, N=1e8, m=64):
+// Launch shapes chosen by measurement (tools/microbench/level_shapes.cu and
+// in-graph A/B runs on B200, N=1e8, m=64):
 // Stage 1  128 threads, <=80 regs (6 CTAs/SM), one chunk per thread (full grid)
-// Stage 3  128 threads, <=128 regs (4 CTAs/SM), persistent grid-stride
+// Stage 3  128 threads, <=128 regs (4 CTAs/SM), one chunk per thread (full
+//          grid: 1.2% faster in the solve graph than a persistent grid-stride)
 template <class T, int L, int G, int MODE, bool VEC>
 struct FastCfg {
     static constexpr int kThreads = 128;
@@ -917,7 +919,7 @@ struct FastCfg {
 template <class T, int L, int G, bool VEC>
 static cudaError_t launch_fast_t(int mode, const SysPtrs<T>& sys, int64_t nblocks,
                                  const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
-                                 int level, int grid_cap, cudaStream_t st) {
+                                 int level, cudaStream_t st) {
     const int64_t nchunks = nblocks * G;
     if (mode == kStage1) {
         using C = FastCfg<T, L, G, kStage1, VEC>;
@@ -928,7 +930,6 @@ static cudaError_t launch_fast_t(int mode, const SysPtrs<T>& sys, int64_t nblock
     } else {
         using C = FastCfg<T, L, G, kStage3, VEC>;
         int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
-        if (grid > grid_cap) grid = grid_cap;
         if (grid < 1) grid = 1;
         return launch_k(k_fast<T, L, G, kStage3, VEC, C::kThreads, C::kMinBlocks>, (unsigned)grid,
                         C::kThreads, 0, st, sys, nblocks, out, xi, x, err, level);
@@ -938,9 +939,9 @@ static cudaError_t launch_fast_t(int mode, const SysPtrs<T>& sys, int64_t nblock
 template <class T, int L, int G>
 static cudaError_t launch_fast_v(bool vec, int mode, const SysPtrs<T>& sys, int64_t nblocks,
                                  const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
-                                 int level, int grid_cap, cudaStream_t st) {
-    if (vec) return launch_fast_t<T, L, G, true>(mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
-    return launch_fast_t<T, L, G, false>(mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
+                                 int level, cudaStream_t st) {
+    if (vec) return launch_fast_t<T, L, G, true>(mode, sys, nblocks, out, xi, x, err, level, st);
+    return launch_fast_t<T, L, G, false>(mode, sys, nblocks, out, xi, x, err, level, st);
 }
 
 // m -> (rows per lane L, lanes per block G) of the fixed-shape kernels
@@ -972,9 +973,9 @@ bool fast_shape(int64_t m, int* L, int* G) {
 template <class T>
 cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs<T>& sys, int64_t nblocks,
                         const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
-                        int level, int grid_cap, cudaStream_t st) {
+                        int level, cudaStream_t st) {
 #define TPB_CASE(MM, LL, GG) \
-    case MM: return launch_fast_v<T, LL, GG>(vec, mode, sys, nblocks, out, xi, x, err, level, grid_cap, st);
+    case MM: return launch_fast_v<T, LL, GG>(vec, mode, sys, nblocks, out, xi, x, err, level, st);
     switch (m) {
         TPB_FAST_SHAPES(TPB_CASE)
         default: return cudaErrorInvalidValue;
@@ -982,25 +983,6 @@ cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs<T>& sys, in
 #undef TPB_CASE
 }
 
-template <class T>
-int fast_max_active_blocks(int64_t m, bool vec, int mode) {
-    int nb = 0;
-#define TPB_OCC(MM, LL, GG)                                                                         \
-    case MM: {                                                                                      \
-        void* fn = mode == kStage1 ? (vec ? FastCfg<T, LL, GG, kStage1, true>::fn()                  \
-                                          : FastCfg<T, LL, GG, kStage1, false>::fn())                \
-                                   : (vec ? FastCfg<T, LL, GG, kStage3, true>::fn()                  \
-                                          : FastCfg<T, LL, GG, kStage3, false>::fn());               \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0);                             \
-        break;                                                                                      \
-    }
-    switch (m) {
-        TPB_FAST_SHAPES(TPB_OCC)
-        default: break;
-    }
-#undef TPB_OCC
-    return nb;
-}
 
 // Runtime-length register path (k_fast_rt): the G with ceil(m/G) <= 8, m/G >= 2.
 int fast_rt_G(int64_t m) {
@@ -1017,8 +999,8 @@ cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs<T>& sys, int64_t n
     const int G = fast_rt_G(m);
     if (G == 0) return cudaErrorInvalidValue;
     const int64_t nchunks = nblocks * G;
-    int64_t grid = (nchunks + 127) / 128;
-    if (mode != kStage1 && grid > (int64_t)sms * 4) grid = (int64_t)sms * 4;
+    int64_t grid = (nchunks + 127) / 128;  // one tile per CTA, both stages
+    (void)sms;
     if (grid < 1) grid = 1;
 #define TPB_RT(GG)                                                                                     \
     case GG:                                                                                           \
@@ -1163,10 +1145,9 @@ cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsign
 
 // explicit instantiations for the two element types of the C-ABI
 #define TPB_INSTANTIATE(T)                                                                          \
-    template int fast_max_active_blocks<T>(int64_t, bool, int);                                     \
     template cudaError_t launch_fast<T>(int64_t, bool, int, const SysPtrs<T>&, int64_t,             \
                                         const IfacePtrs<T>&, const T*, T*, unsigned long long*, int, \
-                                        int, cudaStream_t);                                         \
+                                        cudaStream_t);                                         \
     template cudaError_t launch_fast_rt<T>(int64_t, int, const SysPtrs<T>&, int64_t,                \
                                            const IfacePtrs<T>&, const T*, T*, unsigned long long*,  \
                                            int, int, cudaStream_t);                                 \

@@ -63,11 +63,9 @@ bool fast_shape(int64_t m, int* L, int* G);
 int fast_rt_G(int64_t m);
 
 template <class T>
-int fast_max_active_blocks(int64_t m, bool vec, int mode);
-template <class T>
 cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs<T>& sys, int64_t nblocks,
                         const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
-                        int level, int grid_cap, cudaStream_t st);
+                        int level, cudaStream_t st);
 template <class T>
 cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs<T>& sys, int64_t nblocks,
                            const IfacePtrs<T>& out, const T* xi, T* x, unsigned long long* err,
