@@ -32,6 +32,7 @@ UNIT = "unknowns/s"
 ALG_BYTES_PER_UNKNOWN = 40.0   # read sub/diag/super/rhs once + write x once
 TWO_PASS_BYTES_PER_UNKNOWN = 72.0  # compulsory for an exact two-pass solve once 32N >> L2
 FALLBACK_HBM_GBS = 6650.0
+PATTERN_CEILING_GBS = 7191.0  # read 4 + write 1 FP64 streams, full grid (tools/microbench/stream_ceiling.cu)
 
 
 def parse():
@@ -107,18 +108,26 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.001)
 
     def __enter__(self):
+        # the launch loop holds the GIL between ctypes calls: switch threads
+        # often so the sampler sees the whole (short) timed region
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(2e-4)
         if self.ok:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            t_wait = time.perf_counter() + 0.2
+            while not self.samples and time.perf_counter() < t_wait:
+                time.sleep(1e-4)  # first sample taken before the timed region starts
         return self
 
     def __exit__(self, *a):
         self.stop_flag = True
         if self.ok:
             self.t.join()
+        sys.setswitchinterval(self._switch)
 
     def summary(self):
         if not self.ok or not self.samples:
@@ -424,6 +433,10 @@ def run_ours(args):
                     traffic = None
             roof = {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic,
+                    "peak_note": ("peak = the driver's copy bandwidth (1 read : 1 write); this kernel streams "
+                                  "4 reads : 1 write, whose measured B200 ceiling with trivial compute is "
+                                  f"{PATTERN_CEILING_GBS:.0f} GB/s (profiles/r01_microbench.md)"),
+                    "frac_of_pattern_ceiling": achieved / PATTERN_CEILING_GBS,
                     "alg_bytes_per_launch": ALG_BYTES_PER_UNKNOWN * n_loc,
                     "kernel_ms": t_k, "peak_source": peak_src,
                     "kernel_share_of_step": t_k / sum(prof.values())}
