@@ -15,6 +15,8 @@ import time
 import numpy as np
 import pytest
 
+from conftest import needs_shared_gpu
+
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -56,6 +58,7 @@ def _ok(m):
     return m["finite"] and m["d"] <= TOL_NORM and m["f"] <= TOL_FLOOR and m["r"] <= TOL_RES
 
 
+@needs_shared_gpu
 @pytest.mark.parametrize("P", [1, 2, 3, 8])
 def test_fused_sharded_simulated_ranks(tp, P):
     m = _run_sim(_METRICS + f"""
@@ -68,6 +71,7 @@ print(json.dumps(metrics(s, x, ref)))
     assert _ok(m), m
 
 
+@needs_shared_gpu
 def test_fused_sharded_knn_policy_and_repeats(tp):
     """kNN policy of the global N (recursion levels on every shard); three
     back-to-back solves on the same links alternate the mailbox slots and
@@ -85,6 +89,7 @@ print(json.dumps({"m": out, "same": bool(np.array_equal(xs[0], xs[1]) and np.arr
     assert m["same"]
 
 
+@needs_shared_gpu
 def test_fused_matches_nccl_path_algebra(tp):
     """Fused and host-gathered paths compute the same top system: results
     agree to rounding."""
@@ -177,6 +182,7 @@ def _ipc_worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
+@needs_shared_gpu
 def test_fused_two_processes_cuda_ipc(tp, oracle_mod):
     import torch.multiprocessing as mp
 
@@ -200,6 +206,7 @@ def test_fused_two_processes_cuda_ipc(tp, oracle_mod):
     _check(oracle_mod, s, x, ref)
 
 
+@needs_shared_gpu
 @pytest.mark.parametrize("world,transport", [(2, "auto"), (3, "nccl")])
 def test_bench_multi_rank_flow_on_one_gpu(world, transport):
     """bench.py's N>1 path (torchrun, one process per rank, sharded solve,

@@ -13,6 +13,8 @@ import os
 import numpy as np
 import pytest
 
+from conftest import needs_shared_gpu
+
 pytestmark = pytest.mark.gpu
 
 TOL_NORM = 1e-10
@@ -350,6 +352,7 @@ def test_async_host_solves_on_two_contexts(tp, oracle_mod):
         c.close()
 
 
+@needs_shared_gpu
 def test_single_cta_finishing_solve_still_matches(tp):
     """TPB_FINAL_CLUSTER=0 keeps the single-CTA k_final (the default is the
     8-CTA cluster kernel for systems >= 64 rows); both must pass parity."""
