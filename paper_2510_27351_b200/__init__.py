@@ -5,7 +5,8 @@ from .tridpart import (  # noqa: F401
     Error, HeuristicModel, InvalidSizeError, KTooLargeError, MalformedHeaderError, Observation,
     ObservationSet, PartitionPlan, RecursionPolicy, SchemaError, TrainingPair, Tridiagonal,
     TridiagonalSystem, VersionMismatchError, ZeroPivotError, check_device_error, context,
-    default_depth_model, default_fp32_size_model, default_size_model, fit_depth_model, fit_knn, generate_system,
+    b200_size_model, default_depth_model, default_fp32_size_model, default_size_model, fit_depth_model, fit_knn,
+    generate_system,
     kMaxRecursionDepth, kModelFormatVersion, kPivotFloor, load_model, make_plan, plan_levels,
     predict, predicted_policy, read_observations, recursion_sizes, residual_inf, save_model,
     solve_partition, solve_partition_async, thomas_solve, torch_stream)

@@ -578,6 +578,16 @@ def default_depth_model() -> HeuristicModel:
     return _bundled(1)
 
 
+def b200_size_model() -> HeuristicModel:
+    """The m-predictor re-fitted on the B200 (config 5): fit_knn(k=1) of the
+    plateau-corrected sweep_m observations in profiles/r01_sweep_b200.csv
+    (heuristics/b200_fp64_size_model.json). Device-specific, as the paper
+    expects; the reference-parity default stays
+    default_size_model()."""
+    return load_model(os.path.join(os.path.dirname(os.path.abspath(__file__)), "heuristics",
+                                   "b200_fp64_size_model.json"))
+
+
 def predicted_policy(n: int, size_model: Optional[HeuristicModel] = None,
                      depth_model: Optional[HeuristicModel] = None) -> RecursionPolicy:
     """recursion_sizes(N, predict(depth_model, N), size_model) — the policy the
