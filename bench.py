@@ -404,6 +404,10 @@ def run_ours(args):
         if sync_ms is not None:
             e2e["sync_call_ms"] = sync_ms
             e2e["sync_call_value"] = n_glob / (sync_ms * 1e-3)
+        # what came back over PCIe is the solution: same kernels on the same
+        # inputs as the device-resident steps, so it must match them bit for bit
+        e2e["result_matches_device_solve"] = bool(torch.equal(hx[(args.e2e_steps - 1) % 2 if not sharded_mode
+                                                                  else 0], x.cpu()))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
