@@ -23,6 +23,7 @@
 
 #include "../../include/tridpart_b200.h"
 #include "tp_kernels.h"
+#include "tp_stage.h"
 
 using tpb::IfacePtrs;
 using tpb::SysPtrs;
@@ -201,6 +202,7 @@ struct tp_ctx {
     int64_t link_gen = 0;
     std::vector<void*> ipc_opened;
     bool prepare_only = false;  // capture + instantiate the graph, do not launch
+    tpb::Stager stager;         // pinned staging of pageable host buffers
     void* dsys = nullptr;                 // host-path staging (5 arrays)
     size_t dsys_cap = 0;                  // bytes
     int64_t last_launches = 0;
@@ -543,13 +545,21 @@ tp_status host_roundtrip(tp_ctx* ctx, const T* sub, const T* diag, const T* supe
     if (s != TP_OK) return s;
     const cudaStream_t st = stream ? stream : ctx->stream;
     const size_t bytes = (size_t)n * sizeof(T);
-    TP_CUDA(cudaMemcpyAsync(d[0], sub, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(d[1], diag, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(d[2], super, bytes, cudaMemcpyHostToDevice, st));
-    TP_CUDA(cudaMemcpyAsync(d[3], rhs, bytes, cudaMemcpyHostToDevice, st));
+    // pinned buffers: direct DMA; pageable ones (synchronous calls): staged
+    // through the context's pinned chunks by host threads (tp_stage.h)
+    const T* in[4] = {sub, diag, super, rhs};
+    for (int i = 0; i < 4; ++i) {
+        if (async || tpb::is_pinned_host(in[i]))
+            TP_CUDA(cudaMemcpyAsync(d[i], in[i], bytes, cudaMemcpyHostToDevice, st));
+        else
+            TP_CUDA(ctx->stager.h2d(d[i], in[i], bytes, st));
+    }
     s = body(d, st);
     if (s != TP_OK) return s;
-    TP_CUDA(cudaMemcpyAsync(x, d[4], bytes, cudaMemcpyDeviceToHost, st));
+    if (async || tpb::is_pinned_host(x))
+        TP_CUDA(cudaMemcpyAsync(x, d[4], bytes, cudaMemcpyDeviceToHost, st));
+    else
+        TP_CUDA(ctx->stager.d2h(x, d[4], bytes, st));
     if (async) return TP_OK;
     TP_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     TP_CUDA(cudaStreamSynchronize(st));

@@ -393,3 +393,19 @@ def test_zero_pivot_in_the_finishing_solve(tp, n):
         d[row] = 0.0
         with pytest.raises(tp.ZeroPivotError):
             tp.thomas_solve(tp.TridiagonalSystem(sub, d, sup, rhs))
+
+
+def test_pageable_and_pinned_host_buffers_give_identical_results(tp, oracle_mod):
+    """The host-pointer solve stages pageable buffers through pinned 64 MB
+    chunks (host threads + DMA, tp_stage.h) and DMAs pinned ones directly:
+    same bits either way, across chunk boundaries (n * 8 B > 64 MB, ragged)."""
+    import torch
+
+    n = 9_000_001
+    s = oracle_mod.generate_system(n, 17)
+    pol = tp.RecursionPolicy([64, 10])
+    x_pageable = tp.solve_partition(tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs), pol)
+    pinned = [torch.from_numpy(a).pin_memory() for a in (s.sub, s.diag, s.sup, s.rhs)]
+    x_pinned = tp.solve_partition(tp.TridiagonalSystem(*(t.numpy() for t in pinned)), pol)
+    assert np.array_equal(x_pageable, x_pinned)
+    _check(oracle_mod, s, x_pageable, oracle_mod.solve_partition(s, pol.sizes))
