@@ -87,6 +87,15 @@ __device__ __forceinline__ void pdl_begin() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Stage 3 of a level recomputes exactly the sweeps and merges Stage 1 ran on
+// the same rows (bit-identical arithmetic), so every pivot it meets was already
+// checked there: its kernels carry this no-op guard.
+template <class T>
+struct NoGuard {
+    __device__ __forceinline__ void see(T, int64_t) {}
+    __device__ __forceinline__ bool tripped() const { return false; }
+};
+
 // err word encodes (level << 48) | row; atomicMin keeps the lexicographically
 // first failure. Reported to the host as ZeroPivotError(row) at `level`.
 __device__ __forceinline__ void report_pivot(unsigned long long* err, int level, int64_t bad) {

@@ -3,6 +3,8 @@
 //   k_fast<T,L,G,MODE>       one partition level, full blocks of m = L*G rows
 //   k_fast_rt<T,LMAX,G,MODE> one partition level, any m <= LMAX*G (runtime)
 #pragma once
+#include <type_traits>
+
 #include "tp_device.cuh"
 
 namespace tpb {
@@ -18,7 +20,8 @@ struct LaneState {
     T rbeta[KEEP ? L : 1], gam[KEEP ? L : 1], del[KEEP ? L : 1];
     MergeSave<T> sv[LOGG > 0 ? LOGG : 1];
     Eq2<T> cur;
-    MinGuard<T> guard;
+    // Stage 1 checks every pivot; Stage 3 repeats the same arithmetic (NoGuard)
+    typename std::conditional<KEEP, NoGuard<T>, MinGuard<T>>::type guard;
 };
 
 template <class T, int L, bool VEC>
