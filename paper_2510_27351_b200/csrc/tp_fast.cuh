@@ -101,7 +101,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int64_t nchunks = nblocks * G;
     const int lane = threadIdx.x & 31;
     const int c = lane % G;  // chunk index inside the block
-    int64_t bad = INT64_MAX;
     pdl_begin();
 
     for (int64_t base = (int64_t)blockIdx.x * THREADS; base < nchunks;
@@ -127,20 +126,17 @@ __global__ void __launch_bounds__(THREADS, MINB)
         lanes_tree<T, L, G, KEEP>(s, c, row0);
         if constexpr (MODE == kStage1) {
             if (active) {
-                if (s.guard.tripped()) bad = row0 < bad ? row0 : bad;
+                // rare: report at once instead of carrying a row across the loop
+                if (s.guard.tripped()) report_pivot(err, level, row0);
                 if (c == 0) store_block_eqs(out, blk, s.cur);
             }
         } else {
             T xv[L];
             lanes_tree_down<T, L, G>(s, c, xs, xe);
             leaf_expand<T, L, L>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv);
-            if (active) {
-                if (s.guard.tripped()) bad = row0 < bad ? row0 : bad;
-                store_rows<T, L, VEC>(x, row0, xv);
-            }
+            if (active) store_rows<T, L, VEC>(x, row0, xv);  // pivots: checked by Stage 1
         }
     }
-    report_pivot(err, level, bad);
 }
 
 // ===========================================================================
@@ -161,7 +157,6 @@ __global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
     const int llo = (int)(m / G), ext = (int)(m % G);
     const int len = llo + (c < ext ? 1 : 0);
     const int off = c * llo + (c < ext ? c : ext);
-    int64_t bad = INT64_MAX;
     pdl_begin();
 
     for (int64_t base = (int64_t)blockIdx.x * THREADS; base < nchunks;
@@ -201,7 +196,7 @@ __global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
         lanes_tree<T, LMAX, G, KEEP>(s, c, row0);
         if constexpr (MODE == kStage1) {
             if (active) {
-                if (s.guard.tripped()) bad = row0 < bad ? row0 : bad;
+                if (s.guard.tripped()) report_pivot(err, level, row0);  // rare: report at once
                 if (c == 0) store_block_eqs(out, blk, s.cur);
             }
         } else {
@@ -216,15 +211,13 @@ __global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
                 case 7: leaf_expand<T, LMAX, 7>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
                 default: leaf_expand<T, LMAX, LMAX>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv); break;
             }
-            if (active) {
-                if (s.guard.tripped()) bad = row0 < bad ? row0 : bad;
+            if (active) {  // pivots: checked by Stage 1
 #pragma unroll
                 for (int i = 0; i < LMAX; ++i)
                     if (i < len) x[row0 + i] = xv[i];
             }
         }
     }
-    report_pivot(err, level, bad);
 }
 
 }  // namespace tpb
