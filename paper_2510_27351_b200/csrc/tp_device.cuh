@@ -96,6 +96,13 @@ struct NoGuard {
     __device__ __forceinline__ bool tripped() const { return false; }
 };
 
+// The same for the RowGuard-based (generic / finishing) kernels.
+struct NoRowGuard {
+    static constexpr int64_t bad = INT64_MAX;
+    template <class T>
+    __device__ __forceinline__ void see(T, int64_t) {}
+};
+
 // err word encodes (level << 48) | row; atomicMin keeps the lexicographically
 // first failure. Reported to the host as ZeroPivotError(row) at `level`.
 __device__ __forceinline__ void report_pivot(unsigned long long* err, int level, int64_t bad) {

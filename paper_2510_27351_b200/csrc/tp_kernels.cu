@@ -12,6 +12,7 @@
 //   k_residual           residual_inf (tridiagonal.hpp:74-87)
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <cooperative_groups.h>
@@ -53,9 +54,8 @@ struct GenShared {
 
 // Leaf on a shared-memory chunk [p, p+len). When KEEP, overwrites b <- rcp(beta),
 // c <- gamma, d <- delta for the interior rows (consumed by leaf expansion).
-template <class T, bool KEEP>
-__device__ Eq2<T> leaf_smem(T* a, T* b, T* c, T* d, int len, int64_t grow0,
-                         RowGuard& bad) {
+template <class T, bool KEEP, class Gd>
+__device__ Eq2<T> leaf_smem(T* a, T* b, T* c, T* d, int len, int64_t grow0, Gd& bad) {
     Eq2<T> q;
     if (len == 1) {  // only in the n == 1 solve
         q.a1 = a[0]; q.b1 = b[0]; q.g1 = c[0]; q.d1 = d[0];
@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs<T> sys, int64
     const int64_t off = c * Llo + (c < ext ? c : ext);
     int logg = 0;
     while ((1 << logg) < G) ++logg;
-    RowGuard bad;
+    // Stage 3 repeats Stage 1's arithmetic on the same rows: no pivot guard
+    typename std::conditional<MODE == kStage3, NoRowGuard, RowGuard>::type bad;
     constexpr bool KEEP = (MODE != kStage1);
     pdl_begin();
 
