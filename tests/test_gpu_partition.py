@@ -409,3 +409,21 @@ def test_pageable_and_pinned_host_buffers_give_identical_results(tp, oracle_mod)
     x_pinned = tp.solve_partition(tp.TridiagonalSystem(*(t.numpy() for t in pinned)), pol)
     assert np.array_equal(x_pageable, x_pinned)
     _check(oracle_mod, s, x_pageable, oracle_mod.solve_partition(s, pol.sizes))
+
+
+def test_randomized_sizes_and_policies_against_the_oracle(tp, oracle_mod):
+    """400 random (N, policy) pairs: N log-uniform in [2, 4e5], depth 0..3,
+    every m in [2, 400] (fixed-shape, runtime-length and generic level
+    kernels, every tail length, single-CTA and cluster finishing solves,
+    device-internal levels), each against the oracle's solve_partition."""
+    rng = np.random.default_rng(20261017)
+    for case in range(400):
+        n = int(np.exp(rng.uniform(np.log(2), np.log(4e5))))
+        depth = int(rng.integers(0, 4))
+        sizes = [int(rng.integers(2, 401)) for _ in range(depth + 1)]
+        s = oracle_mod.generate_system(n, 1000 + case)
+        ref = oracle_mod.solve_partition(s, sizes)
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes))
+        d = oracle_mod.rel_inf_diff(x, ref)
+        r = oracle_mod.residual_inf(s, x)
+        assert np.all(np.isfinite(x)) and d <= TOL_NORM and r <= TOL_RES, (case, n, sizes, d, r)
