@@ -230,3 +230,27 @@ def test_bench_multi_rank_flow_on_one_gpu(world, transport):
     assert d["n_gpus"] == world and d["config"]["n_global"] == 4_000_000 * world
     assert d["config"]["transport"] == ("p2p" if transport == "auto" else "nccl")
     assert d["residual"] <= 1e-12 and d["value"] > 0 and d["gpu_launches"] > 0
+
+
+@needs_shared_gpu
+def test_fused_random_shards_including_tiny_ones(tp):
+    """Random global sizes (down to 2 rows per shard), rank counts and
+    policies: the finishing kernel takes the single-CTA path for shards whose
+    deepest system is under 64 rows and the cluster path above, in every mode."""
+    m = _run_sim(_METRICS + """
+rng = np.random.default_rng(7)
+out = []
+for case in range(24):
+    P = int(rng.integers(1, 7))
+    n = int(np.exp(rng.uniform(np.log(2 * P), np.log(3e5))))
+    sizes = [int(rng.integers(2, 80)) for _ in range(int(rng.integers(1, 3)))]
+    s = oracle.generate_system(n, 500 + case)
+    ref = oracle.solve_partition(s, sizes)
+    x = sharded.simulate_ranks_fused(s.sub, s.diag, s.sup, s.rhs, P, sizes)
+    mm = metrics(s, x, ref)
+    mm.update(P=P, n=n, sizes=sizes)
+    out.append(mm)
+print(json.dumps(out))
+""")
+    bad = [c for c in m if not _ok(c)]
+    assert not bad, bad
