@@ -80,3 +80,17 @@ def test_fp32_observer_and_thomas(tp, oracle_mod):
         assert np.all(np.abs(f.diag) >= np.abs(f.sub) + np.abs(f.super) - 1e-5)
     xt = tp.thomas_solve(tp.TridiagonalSystem(a, b, c, d))
     assert oracle_mod.residual_inf_f32(a, b, c, d, xt) <= TOL32
+
+
+def test_fp32_randomized_sizes_and_policies(tp, oracle_mod):
+    """120 random (N, policy) pairs in FP32 against the reference's own
+    solve_partition<float> (oracle/_ref) and the FP64 oracle."""
+    rng = np.random.default_rng(3232)
+    for case in range(120):
+        n = int(np.exp(rng.uniform(np.log(4), np.log(2e5))))
+        sizes = [int(rng.integers(2, 300)) for _ in range(int(rng.integers(1, 4)))]
+        a, b, c, d = _f32_system(n, 7000 + case)
+        x = tp.solve_partition(tp.TridiagonalSystem(a, b, c, d), tp.RecursionPolicy(sizes))
+        assert np.all(np.isfinite(x)), (case, n, sizes)
+        assert oracle_mod.residual_inf_f32(a, b, c, d, x) <= TOL32, (case, n, sizes)
+        assert _rel(x, oracle_mod.solve_partition_f32(a, b, c, d, sizes)) <= TOL32, (case, n, sizes)
