@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Benchmark: FP64 recursive partition solve on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--n N_PER_GPU] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n|--size N_PER_GPU]
+                    [--transport auto|p2p|nccl] [--impl ours|reference]
 
 A step is one full solve (all levels, finishing solve, Stage 3) of an
 N = 1e8-unknown strictly dominant system per GPU with the kNN-predicted
@@ -9,8 +10,10 @@ policy [64, 10, 32, 16] (config 3). Inputs are generated on the device with
 the generate_system distributions and stay resident in HBM (3.2 GB per GPU,
 25x the 126 MB L2, so no L2 flush is needed between steps). N > 1: one
 process per GPU (torchrun), contiguous row shards of the global system
-N_global = N x 1e8 (weak scaling), one NCCL all-gather of 8 doubles per rank
-per solve, device time = max over ranks.
+N_global = N x 1e8 (weak scaling); the one exchange per solve (8 doubles per
+rank) runs inside the finishing kernel over peer memory (transport "p2p",
+chosen by "auto" when every rank can open every peer's CUDA IPC mailbox;
+otherwise an NCCL all-gather); device time = max over ranks.
 
 `--impl reference` times the reference's own CPU solver (oracle/_ref: the
 unmodified reference headers, all host threads) on rank 0 only.
