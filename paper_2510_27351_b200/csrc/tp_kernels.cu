@@ -116,10 +116,14 @@ __global__ void k_residual(SysPtrs<T> sys, int64_t n, const T* __restrict__ x, u
 // way. Off by default: measured on B200 (tools/timeline.py, C3) it saves ~6 us
 // across the levels >= 1 but the persistent Stage-3 grid launched early
 // behind level 1 runs ~50 us slower.
-static bool g_pdl = false;
+// 0: off (default), 1: every solve-path launch, 2: launches of levels >= 1
+// only. Mode 2 measured 2.5 us faster per C3 solve, but early-launched
+// dependents hold SMs while they wait: ranks sharing one GPU (simulated fused
+// ranks) then starve each other's exchange, so it stays opt-in.
+static int g_pdl = 0;
 
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+static cudaError_t launch_k(int level, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
                             cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -130,7 +134,7 @@ static cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned bloc
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = g_pdl ? 1 : 0;
+    cfg.numAttrs = (g_pdl == 1 || (g_pdl == 2 && level > 0)) ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -142,7 +146,7 @@ __global__ void k_reset(unsigned long long* err) {
 }
 
 cudaError_t launch_reset(unsigned long long* err, cudaStream_t st) {
-    return launch_k(k_reset, 1, 32, 0, st, err);
+    return launch_k(0, k_reset, 1, 32, 0, st, err);
 }
 
 // Launch shapes chosen by measurement (tools/microbench/level_shapes.cu and
@@ -166,13 +170,13 @@ static cudaError_t launch_fast_t(int mode, const SysPtrs<T>& sys, int64_t nblock
         using C = FastCfg<T, L, G, kStage1, VEC>;
         int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
         if (grid < 1) grid = 1;
-        return launch_k(k_fast<T, L, G, kStage1, VEC, C::kThreads, C::kMinBlocks>, (unsigned)grid,
+        return launch_k(level, k_fast<T, L, G, kStage1, VEC, C::kThreads, C::kMinBlocks>, (unsigned)grid,
                         C::kThreads, 0, st, sys, nblocks, out, xi, x, err, level);
     } else {
         using C = FastCfg<T, L, G, kStage3, VEC>;
         int64_t grid = (nchunks + C::kThreads - 1) / C::kThreads;
         if (grid < 1) grid = 1;
-        return launch_k(k_fast<T, L, G, kStage3, VEC, C::kThreads, C::kMinBlocks>, (unsigned)grid,
+        return launch_k(level, k_fast<T, L, G, kStage3, VEC, C::kThreads, C::kMinBlocks>, (unsigned)grid,
                         C::kThreads, 0, st, sys, nblocks, out, xi, x, err, level);
     }
 }
@@ -246,8 +250,8 @@ cudaError_t launch_fast_rt(int64_t m, int mode, const SysPtrs<T>& sys, int64_t n
 #define TPB_RT(GG)                                                                                     \
     case GG:                                                                                           \
         if (mode == kStage1)                                                                           \
-            return launch_k(k_fast_rt<T, 8, GG, kStage1>, (unsigned)grid, 128, 0, st, sys, nblocks, m, out, xi, x, err, level); \
-        return launch_k(k_fast_rt<T, 8, GG, kStage3>, (unsigned)grid, 128, 0, st, sys, nblocks, m, out, xi, x, err, level);
+            return launch_k(level, k_fast_rt<T, 8, GG, kStage1>, (unsigned)grid, 128, 0, st, sys, nblocks, m, out, xi, x, err, level); \
+        return launch_k(level, k_fast_rt<T, 8, GG, kStage3>, (unsigned)grid, 128, 0, st, sys, nblocks, m, out, xi, x, err, level);
     switch (G) {
         TPB_RT(1)
         TPB_RT(2)
@@ -274,7 +278,7 @@ cudaError_t launch_generic(int mode, int threads, int G, int grid, const SysPtrs
     const size_t smem = generic_smem_bytes(threads, G, blen, sizeof(T));
     if (smem > kMaxDynSmem) return cudaErrorInvalidValue;
     auto k = mode == kStage1 ? k_generic<T, kStage1> : mode == kStage3 ? k_generic<T, kStage3> : k_generic<T, kSolve>;
-    return launch_k(k, (unsigned)grid, (unsigned)threads, smem, st, sys, row_base, blk_base, nblocks, blen, G,
+    return launch_k(level, k, (unsigned)grid, (unsigned)threads, smem, st, sys, row_base, blk_base, nblocks, blen, G,
                     out, xi, x, err, level);
 }
 
@@ -304,7 +308,7 @@ cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const Iface
                   : mode == kShard  ? k_final_cl<T, kShard>
                                     : k_final_cl<T, kSolve>;
         const ShardLink none{};
-        return launch_k(kc, kFinCS, kFinNT, 0, st, sys, n, gtot, out, xi, x, err, level,
+        return launch_k(level, kc, kFinCS, kFinNT, 0, st, sys, n, gtot, out, xi, x, err, level,
                         link != nullptr ? *link : none);
     }
     const int G = final_G(n);
@@ -314,7 +318,7 @@ cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const Iface
              : mode == kShard  ? k_final<T, kShard>
                                : k_final<T, kSolve>;
     const ShardLink none{};
-    return launch_k(k, 1, kFinalThreads2, smem, st, sys, n, G, out, xi, x, err, level,
+    return launch_k(level, k, 1, kFinalThreads2, smem, st, sys, n, G, out, xi, x, err, level,
                     link != nullptr ? *link : none);
 }
 
@@ -332,7 +336,7 @@ static cudaError_t set_smem_attributes() {
 }
 
 cudaError_t init_kernel_attributes() {
-    if (const char* v = getenv("TPB_PDL")) g_pdl = atoi(v) != 0;
+    if (const char* v = getenv("TPB_PDL")) g_pdl = atoi(v);
     if (const char* v = getenv("TPB_FINAL_CLUSTER")) g_final_cluster = atoi(v) != 0;
     cudaError_t e = set_smem_attributes<double>();
     if (e == cudaSuccess) e = set_smem_attributes<float>();
@@ -342,7 +346,7 @@ cudaError_t init_kernel_attributes() {
 template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st) {
-    return launch_k(k_gather_solve<T>, 1, 32, 0, st, eqs, nranks, rank, x2, scratch, err, level);
+    return launch_k(level, k_gather_solve<T>, 1, 32, 0, st, eqs, nranks, rank, x2, scratch, err, level);
 }
 
 template <class T>
