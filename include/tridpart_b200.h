@@ -170,6 +170,8 @@ tp_status tp_shard_finish_f64_dev(tp_ctx* ctx, const double* sub, const double* 
  * pairs (bounded spin; timeout -> TP_ERR_NCCL), solves the 2P-row top system
  * (Thomas) and expands -> Stage 3 levels. All ranks must call it the same
  * number of times (the epoch flags pair the calls). */
+/* A call with a different nranks frees and reallocates the mailbox: export,
+ * open and attach again on every rank. */
 tp_status tp_shard_mailbox(tp_ctx* ctx, int32_t nranks, void** mailbox, tp_error* err);
 tp_status tp_ipc_get_handle(tp_ctx* ctx, void* dev_ptr, uint8_t* handle64, tp_error* err);
 tp_status tp_ipc_open_handle(tp_ctx* ctx, const uint8_t* handle64, void** dev_ptr, tp_error* err);

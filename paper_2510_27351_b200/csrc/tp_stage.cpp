@@ -40,11 +40,17 @@ void HostPool::loop(int id) {
     }
 }
 
+HostPool& HostPool::shared() {
+    static HostPool pool((int)std::max(1u, std::min(std::thread::hardware_concurrency(), 16u)));
+    return pool;
+}
+
 void HostPool::run(int parts, const std::function<void(int)>& fn) {
     if (workers_.empty() || parts <= 1) {
         for (int p = 0; p < parts; ++p) fn(p);
         return;
     }
+    std::lock_guard<std::mutex> turn(run_mu_);
     {
         std::lock_guard<std::mutex> g(mu_);
         job_ = &fn;
@@ -72,7 +78,6 @@ Stager::~Stager() {
         if (buf_[i]) cudaFreeHost(buf_[i]);
         if (ev_[i]) cudaEventDestroy(ev_[i]);
     }
-    delete pool_;
 }
 
 cudaError_t Stager::ensure() {
@@ -82,15 +87,14 @@ cudaError_t Stager::ensure() {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming);
         if (e != cudaSuccess) return e;
     }
-    const unsigned hc = std::thread::hardware_concurrency();
-    pool_ = new HostPool((int)std::max(1u, std::min(hc, 16u)));
     return cudaSuccess;
 }
 
 void Stager::parallel_copy(void* dst, const void* src, size_t bytes) {
-    const int parts = pool_->size() * 2;
+    HostPool& pool = HostPool::shared();
+    const int parts = pool.size() * 2;
     const size_t per = ((bytes + parts - 1) / parts + 4095) & ~size_t(4095);
-    pool_->run(parts, [&](int p) {
+    pool.run(parts, [&](int p) {
         const size_t lo = std::min(bytes, (size_t)p * per), hi = std::min(bytes, lo + per);
         if (hi > lo) std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
     });

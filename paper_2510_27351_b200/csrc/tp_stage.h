@@ -27,12 +27,16 @@ public:
     HostPool(const HostPool&) = delete;
     HostPool& operator=(const HostPool&) = delete;
     int size() const { return (int)workers_.size() + 1; }
-    // fn(part) for part in [0, parts), the caller runs part 0
+    // fn(part) for part in [0, parts), the caller runs part 0; calls from
+    // several host threads take turns (one job at a time)
     void run(int parts, const std::function<void(int)>& fn);
+    // the process-wide pool every context's Stager shares
+    static HostPool& shared();
 
 private:
     void loop(int id);
     std::vector<std::thread> workers_;
+    std::mutex run_mu_;
     std::mutex mu_;
     std::condition_variable cv_, done_cv_;
     const std::function<void(int)>* job_ = nullptr;
@@ -60,7 +64,6 @@ private:
     static constexpr size_t kChunk = size_t(64) << 20;
     void* buf_[2] = {nullptr, nullptr};
     cudaEvent_t ev_[2] = {nullptr, nullptr};
-    HostPool* pool_ = nullptr;
 };
 
 // true when `p` is page-locked (cudaMallocHost / cudaHostRegister) memory
