@@ -195,3 +195,31 @@ def test_model_json_roundtrip_and_schema(tp, tmp_path):
     path.write_text("{not json")
     with pytest.raises(tp.SchemaError):
         tp.load_model(str(path))
+
+
+def test_shard_entries_reject_bad_arguments_without_a_device(tp):
+    """The multi-GPU entries validate their arguments before touching CUDA:
+    NULL context / NULL outputs / bad rank counts give TP_ERR_INVALID_ARGUMENT
+    (the status the Python layer maps to ValueError), never a crash."""
+    import ctypes as C
+
+    from paper_2510_27351_b200 import _lib
+    from paper_2510_27351_b200._lib import TpError
+
+    lib, INV = _lib.lib, _lib.INVALID_ARGUMENT
+    err = TpError()
+    box = C.c_void_p()
+    h = (C.c_uint8 * 64)()
+    assert lib.tp_shard_mailbox(None, 2, C.byref(box), C.byref(err)) == INV
+    assert lib.tp_ipc_get_handle(None, C.c_void_p(0x1000), h, C.byref(err)) == INV
+    assert lib.tp_ipc_open_handle(None, h, C.byref(box), C.byref(err)) == INV
+    ptrs = (C.c_void_p * 2)()
+    assert lib.tp_shard_attach(None, 2, 0, ptrs, C.byref(err)) == INV
+    sizes = np.array([32], dtype=np.int64)
+    sp = sizes.ctypes.data_as(C.POINTER(C.c_int64))
+    for fn in (lib.tp_shard_solve_f64_dev, lib.tp_shard_prepare_f64_dev):
+        st = fn(None, None, None, None, None, 100, sp, 1, None, None, C.byref(err))
+        assert st == INV, st
+    with pytest.raises(ValueError):
+        from paper_2510_27351_b200.tridpart import _call
+        _call(lib.tp_shard_mailbox, None, 0, C.byref(box))
