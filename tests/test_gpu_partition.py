@@ -428,3 +428,17 @@ def test_randomized_sizes_and_policies_against_the_oracle(tp, oracle_mod):
         d = oracle_mod.rel_inf_diff(x, ref)
         r = oracle_mod.residual_inf(s, x)
         assert np.all(np.isfinite(x)) and d <= TOL_NORM and r <= TOL_RES, (case, n, sizes, d, r)
+
+
+@pytest.mark.skipif(os.environ.get("TPB_SLOW") != "1", reason="set TPB_SLOW=1 (a few minutes)")
+def test_randomized_large_sizes_and_deep_policies(tp, oracle_mod):
+    """60 random (N, policy) pairs with N log-uniform in [4e5, 2e7], depth
+    0..4, m in [2, 400], against the oracle (all three parity gates)."""
+    rng = np.random.default_rng(99)
+    for case in range(60):
+        n = int(np.exp(rng.uniform(np.log(4e5), np.log(2e7))))
+        depth = int(rng.integers(0, 5))
+        sizes = [int(rng.integers(2, 400)) for _ in range(depth + 1)]
+        s = oracle_mod.generate_system(n, 50_000 + case)
+        _check(oracle_mod, s, tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes)),
+               oracle_mod.solve_partition(s, sizes))
