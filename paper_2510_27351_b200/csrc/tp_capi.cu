@@ -307,10 +307,23 @@ struct Runner {
         check(tpb::launch_reset(ctx->d_err, st));
         solve_body(p);
     }
+    // The deepest level and the finishing solve run as one cluster kernel when
+    // that level fits the cluster's shared memory (k_level_final_cl); its
+    // interface system and solution then never touch HBM.
     void solve_body(const Plan<T>& p) {
-        for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
-        final_solve(p);
-        for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
+        const size_t nl = p.levels.size();
+        const bool fuse = nl > 0 && tpb::level_final_fits(p.levels.back().n, p.levels.back().m,
+                                                          p.levels.back().K, sizeof(T));
+        const size_t top = fuse ? nl - 1 : nl;
+        for (size_t l = 0; l < top; ++l) stage(p.levels[l], (int)l, tpb::kStage1);
+        if (fuse) {
+            const Level<T>& L = p.levels.back();
+            check(tpb::launch_level_final<T>(L.in, L.n, L.m, L.K, L.x_out, ctx->d_err, (int)top, st));
+            after("level_final", (int)top);
+        } else {
+            final_solve(p);
+        }
+        for (size_t l = top; l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
     }
 
     // Sharded halves.

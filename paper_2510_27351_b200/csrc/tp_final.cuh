@@ -315,44 +315,36 @@ constexpr int kFinCS = 8;     // CTAs per cluster (portable maximum)
 constexpr int kFinNT = 256;   // threads per CTA
 constexpr int kFinRows = kFinNT * 4;  // rows staged per CTA (chunks <= 4 rows)
 
-template <class T, int MODE>
-__global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
-    k_final_cl(SysPtrs<T> sys, int64_t n, int gtot, IfacePtrs<T> out, const T* __restrict__ xi,
-               T* __restrict__ x, unsigned long long* err, int level, const __grid_constant__ ShardLink link) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    __shared__ T sa[kFinRows], sb[kFinRows], sc[kFinRows], sd[kFinRows];
+// The cluster tree over rows already staged in this CTA's shared memory
+// (sa..sd, `rows` rows starting at system row r0, `per` chunks of 2..4 rows,
+// per a power of two <= kFinNT). cta_row0(c) is CTA c's first system row;
+// the chunking is local to the CTA (its first rows % per chunks get the extra
+// row), which equals k_final_cl's global chunking when every CTA owns the same
+// number of chunks. The solution rows go to xdst[row - xbase].
+template <class T, int MODE, class CtaRow0>
+__device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, const T* sa, const T* sb,
+                                        const T* sc, const T* sd, int64_t r0, int rows, int per,
+                                        CtaRow0 cta_row0, int64_t n, const IfacePtrs<T>& out,
+                                        const T* __restrict__ xi, T* __restrict__ xdst, int64_t xbase,
+                                        RowGuard& bad, unsigned long long* err, int level,
+                                        const ShardLink& link) {
     __shared__ Eq2<T> wroot[kFinNT / 32];
     __shared__ Eq2<T> croot;   // this CTA's root pair, read by CTA 0
     __shared__ T cx[2];        // this CTA's (x_s, x_e), written by CTA 0
     __shared__ T wx[2 * (kFinNT / 32)];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int cta = (int)cl.block_rank();
-    RowGuard bad;
     TP_TRACE_DECL;
-    pdl_begin();
     TP_TRACE(0);
-
-    const int per = gtot / kFinCS;  // chunks owned by this CTA (power of two)
-    const int64_t Llo = n / gtot, ext = n % gtot;
-    auto cstart = [&](int64_t g) { return g * Llo + (g < ext ? g : ext); };
-    const int64_t g0 = (int64_t)cta * per;
-    const int64_t r0 = cstart(g0);
-    const int rows = (int)(cstart(g0 + per) - r0);
-    for (int i = tid; i < rows; i += kFinNT) {
-        sa[i] = __ldg(sys.sub + r0 + i);
-        sb[i] = __ldg(sys.diag + r0 + i);
-        sc[i] = __ldg(sys.sup + r0 + i);
-        sd[i] = __ldg(sys.rhs + r0 + i);
-    }
-    __syncthreads();
     TP_TRACE(1);
+
+    const int Llo = rows / per, ext = rows % per;
+    auto cstart = [&](int c) { return r0 + (int64_t)c * Llo + (c < ext ? c : ext); };
 
     // ---- leaf: this thread's chunk (2..4 rows) in registers ----
     const bool active = tid < per;
-    const int64_t g = g0 + tid;
-    const int len = active ? (int)(Llo + (g < ext ? 1 : 0)) : 2;
-    const int64_t grow = active ? cstart(g) : 0;
+    const int len = active ? Llo + (tid < ext ? 1 : 0) : 2;
+    const int64_t grow = active ? cstart(tid) : 0;
     Chunk<T, 4> r;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -378,7 +370,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         const int h = 1 << lv;
         const Eq2<T> oth = shfl_down_eq(cur, h);
         if (h < per && (lane & (2 * h - 1)) == 0 && tid + h < per)
-            cur = merge(cur, oth, cstart(g + h) - 1, bad, sw[lv]);
+            cur = merge(cur, oth, cstart(tid + h) - 1, bad, sw[lv]);
     }
     const int nwr = per >= 32 ? per / 32 : 1;
     if (lane == 0 && warp < nwr) wroot[warp] = cur;
@@ -395,7 +387,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
             const int h = 1 << lv;
             const Eq2<T> oth = shfl_down_eq(wc, h);
             if (h < nwr && (lane & (2 * h - 1)) == 0 && lane + h < nwr)
-                wc = merge(wc, oth, cstart(g0 + 32 * (lane + h)) - 1, bad, sx[lv]);
+                wc = merge(wc, oth, cstart(32 * (lane + h)) - 1, bad, sx[lv]);
         }
         if (lane == 0) croot = wc;
     }
@@ -413,7 +405,7 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
             const int h = 1 << lv;
             const Eq2<T> oth = shfl_down_eq(cc, h);
             if ((lane & (2 * h - 1)) == 0 && lane + h < kFinCS)
-                cc = merge(cc, oth, cstart((int64_t)per * (lane + h)) - 1, bad, sc3[lv]);
+                cc = merge(cc, oth, cta_row0(lane + h) - 1, bad, sc3[lv]);
         }
         T xs = 0, xe = 0;
         if (lane == 0) {
@@ -465,7 +457,6 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         // CTA 0 read every croot before reaching this barrier; no CTA may exit
         // while its shared memory can still be read
         cl.sync();
-        report_pivot(err, level, bad.bad);
         return;
     }
     cl.sync();
@@ -525,13 +516,225 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         else leaf_expand<T, 4, 4>(r, rb, gm, dl, xs, xe, xv);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            if (i < len) x[grow + i] = xv[i];
+            if (i < len) xdst[grow - xbase + i] = xv[i];
     }
     TP_TRACE(9);
     TP_TRACE(10);
     TP_TRACE(11);
     if (blockIdx.x == 0) TP_TRACE_FLUSH;
+}
+
+template <class T, int MODE>
+__global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
+    k_final_cl(SysPtrs<T> sys, int64_t n, int gtot, IfacePtrs<T> out, const T* __restrict__ xi,
+               T* __restrict__ x, unsigned long long* err, int level, const __grid_constant__ ShardLink link) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ T sa[kFinRows], sb[kFinRows], sc[kFinRows], sd[kFinRows];
+    const int tid = threadIdx.x;
+    const int cta = (int)cl.block_rank();
+    RowGuard bad;
+    pdl_begin();
+
+    const int per = gtot / kFinCS;  // chunks owned by each CTA (power of two)
+    const int64_t Llo = n / gtot, ext = n % gtot;
+    auto gstart = [&](int64_t g) { return g * Llo + (g < ext ? g : ext); };
+    const int64_t r0 = gstart((int64_t)cta * per);
+    const int rows = (int)(gstart((int64_t)(cta + 1) * per) - r0);
+    {  // rows <= 4 * kFinNT: every load of the CTA in flight at once
+        T va[4], vb[4], vc[4], vd[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = tid + u * kFinNT;
+            if (i < rows) {
+                va[u] = __ldg(sys.sub + r0 + i);
+                vb[u] = __ldg(sys.diag + r0 + i);
+                vc[u] = __ldg(sys.sup + r0 + i);
+                vd[u] = __ldg(sys.rhs + r0 + i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = tid + u * kFinNT;
+            if (i < rows) { sa[i] = va[u]; sb[i] = vb[u]; sc[i] = vc[u]; sd[i] = vd[u]; }
+        }
+    }
+    __syncthreads();
+    cl_tree<T, MODE>(cl, sa, sb, sc, sd, r0, rows, per, [&](int c) { return gstart((int64_t)per * c); }, n, out,
+                     xi, x, 0, bad, err, level, link);
     report_pivot(err, level, bad.bad);
+}
+
+// ===========================================================================
+// The last partition level and the finishing solve in ONE cluster kernel.
+// When the deepest level's system fits the cluster's shared memory (C3: level
+// 3, 39K rows; C1: the whole 10K-row system), its Stage 1, the finishing solve
+// of its 2K-row interface and its Stage 3 run here instead of as three kernels
+// (plus the Stage-1/Stage-3 tail branches). CTA c owns level blocks
+// [K c / 8, K (c + 1) / 8): their rows are staged once into shared memory, one
+// thread sweeps one block at a time (leaf_smem, partition.hpp:90-124, the same
+// arithmetic as k_generic with one lane per block), the block's E1/E2 rows are
+// this CTA's rows of the interface (assemble_interface order,
+// partition.hpp:139-149), cl_tree solves the interface across the cluster,
+// and each thread back-substitutes its block from the kept sweep values
+// (partition.hpp:154-173) before one coalesced store. The interface never
+// leaves the SMs. Blocks are padded to an odd stride S >= m + 1 so the
+// one-thread-per-block sweeps are free of bank conflicts.
+// ===========================================================================
+constexpr int kLfMaxBlocks = kFinRows / 2;  // level blocks per CTA (interface chunks <= 4 rows)
+
+// Walks local rows e = tid, tid + kFinNT, ... of a CTA's level rows without
+// dividing: (jj, i) = (e / m, e % m); the tail block's extra row (i == m in
+// the last block) maps to slot (nb - 1, m).
+struct LfSlots {
+    int jj, i, dq, dr, m, nb, S;
+    __device__ LfSlots(int tid, int m_, int nb_, int S_) : m(m_), nb(nb_), S(S_) {
+        jj = tid / m; i = tid - jj * m;
+        dq = kFinNT / m; dr = kFinNT - dq * m;
+    }
+    __device__ __forceinline__ int slot() const { return jj < nb ? jj * S + i : (nb - 1) * S + i + m; }
+    __device__ __forceinline__ void next() {
+        jj += dq; i += dr;
+        if (i >= m) { i -= m; ++jj; }
+    }
+};
+
+// Stage-1 sweeps of one full block of MF rows in registers (both sweeps are
+// independent dependency chains the compiler interleaves), the kept values
+// written back to the block's b / c / d slots in leaf_smem's layout.
+template <class T, int MF>
+__device__ __forceinline__ Eq2<T> lf_sweep_regs(T* a, T* b, T* c, T* d, int64_t row0, RowGuard& bad) {
+    Chunk<T, MF> r;
+#pragma unroll
+    for (int i = 0; i < MF; ++i) { r.a[i] = a[i]; r.b[i] = b[i]; r.c[i] = c[i]; r.d[i] = d[i]; }
+    T rb[MF], gm[MF], dl[MF];
+    const Eq2<T> q = leaf_reduce_keep<T, MF, MF>(r, row0, bad, rb, gm, dl);
+#pragma unroll
+    for (int i = 1; i < MF - 1; ++i) { b[i] = rb[i]; c[i] = gm[i]; d[i] = dl[i]; }
+    return q;
+}
+
+template <class T, int MF>
+__device__ __forceinline__ void lf_expand_regs(T* a, const T* rbp, const T* gp, const T* dp, T xs, T xe) {
+    T av[MF], rb[MF], g[MF], dd[MF];
+#pragma unroll
+    for (int i = 1; i < MF - 1; ++i) { av[i] = a[i]; rb[i] = rbp[i]; g[i] = gp[i]; dd[i] = dp[i]; }
+    T prev = xs;
+#pragma unroll
+    for (int i = 1; i < MF - 1; ++i) {
+        const T xv = (dd[i] - av[i] * prev - g[i] * xe) * rb[i];
+        a[i] = xv;
+        prev = xv;
+    }
+    a[0] = xs;
+    a[MF - 1] = xe;
+}
+
+// MF = m when m is 4, 8 or 16 (register sweeps for the full blocks), else 0.
+template <class T, int MF>
+__global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
+    k_level_final_cl(SysPtrs<T> sys, int64_t n, int m, int64_t K, int S, T* __restrict__ x,
+                     unsigned long long* err, int level) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char lf_raw[];
+    __shared__ T fa[kFinRows], fb[kFinRows], fc[kFinRows], fd[kFinRows], fx[kFinRows];
+    const int tid = threadIdx.x;
+    const int cta = (int)cl.block_rank();
+    const int64_t B0 = K * cta / kFinCS, B1 = K * (cta + 1) / kFinCS;
+    const int nb = (int)(B1 - B0);
+    const int nbmax = (int)((K + kFinCS - 1) / kFinCS);
+    T* la = reinterpret_cast<T*>(lf_raw);
+    T* lb = la + (size_t)nbmax * S;
+    T* lc = lb + (size_t)nbmax * S;
+    T* ld = lc + (size_t)nbmax * S;
+    RowGuard bad_lv, bad_fin;
+    pdl_begin();
+    TP_LF_TRACE(0);
+
+    const int64_t r0 = B0 * m;
+    const int rows = (int)((B1 == K ? n : B1 * m) - r0);
+    // ---- stage: every element as its own cp.async into its padded slot (the
+    // level sits in L2; async copies keep far more of it in flight than
+    // register loads: 8.1K -> 5.0K cycles at C3) ----
+    {
+        LfSlots w(tid, m, nb, S);
+        for (int e = tid; e < rows; e += kFinNT, w.next()) {
+            const int k = w.slot();
+            const T* src[4] = {sys.sub + r0 + e, sys.diag + r0 + e, sys.sup + r0 + e, sys.rhs + r0 + e};
+            T* dst[4] = {la + k, lb + k, lc + k, ld + k};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const unsigned sa_ = (unsigned)__cvta_generic_to_shared(dst[q]);
+                if constexpr (sizeof(T) == 8)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa_), "l"(src[q]) : "memory");
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa_), "l"(src[q]) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    TP_LF_TRACE(1);
+
+    // ---- Stage 1 of the level: one thread per block ----
+    for (int jj = tid; jj < nb; jj += kFinNT) {
+        const int64_t j = B0 + jj;
+        const int len = j == K - 1 ? (int)(n - (K - 1) * m) : m;
+        const int o = jj * S;
+        Eq2<T> q;
+        if (MF > 0 && len == MF) q = lf_sweep_regs<T, (MF > 0 ? MF : 4)>(la + o, lb + o, lc + o, ld + o, j * m, bad_lv);
+        else q = leaf_smem<T, true>(la + o, lb + o, lc + o, ld + o, len, j * m, bad_lv);
+        fa[2 * jj] = q.a1; fa[2 * jj + 1] = q.a2;
+        fb[2 * jj] = q.b1; fb[2 * jj + 1] = q.b2;
+        fc[2 * jj] = q.g1; fc[2 * jj + 1] = q.g2;
+        fd[2 * jj] = q.d1; fd[2 * jj + 1] = q.d2;
+    }
+    __syncthreads();
+    TP_LF_TRACE(2);
+
+    // ---- the interface (2K rows) across the cluster ----
+    int per = 1;
+    while (per * 2 <= kFinNT && per * 2 <= nb) per *= 2;
+    const ShardLink none{};
+    cl_tree<T, kSolve>(cl, fa, fb, fc, fd, 2 * B0, 2 * nb, per,
+                       [&](int c) { return 2 * (K * c / kFinCS); }, 2 * K, IfacePtrs<T>{}, nullptr, fx,
+                       2 * B0, bad_fin, err, level + 1, none);
+    __syncthreads();
+    TP_LF_TRACE(3);
+
+    // ---- Stage 3 of the level: back-substitute each block, then one store ----
+    for (int jj = tid; jj < nb; jj += kFinNT) {
+        const int64_t j = B0 + jj;
+        const int len = j == K - 1 ? (int)(n - (K - 1) * m) : m;
+        const int o = jj * S;
+        T* a = la + o;
+        const T xs = fx[2 * jj], xe = fx[2 * jj + 1];
+        if (MF > 0 && len == MF) {
+            lf_expand_regs<T, (MF > 0 ? MF : 4)>(a, lb + o, lc + o, ld + o, xs, xe);
+            continue;
+        }
+        const T* rb = lb + o;
+        const T* g = lc + o;
+        const T* dd = ld + o;
+        T prev = xs;
+        for (int i = 1; i < len - 1; ++i) {
+            const T xv = (dd[i] - a[i] * prev - g[i] * xe) * rb[i];
+            a[i] = xv;
+            prev = xv;
+        }
+        a[0] = xs;
+        a[len - 1] = xe;
+    }
+    __syncthreads();
+    TP_LF_TRACE(4);
+    {
+        LfSlots w(tid, m, nb, S);
+        for (int e = tid; e < rows; e += kFinNT, w.next()) x[r0 + e] = la[w.slot()];
+    }
+    TP_LF_TRACE(5);
+    report_pivot(err, level, bad_lv.bad);
+    report_pivot(err, level + 1, bad_fin.bad);
 }
 
 // ===========================================================================

@@ -25,12 +25,14 @@ namespace tpb {
 
 // Phase timestamps of the finishing solve (scratch builds with -DTPB_TRACE only).
 #ifdef TPB_TRACE
-__device__ unsigned long long g_trace[16];
+__device__ unsigned long long g_trace[24];  // [0, 12) finishing solve, [12, 18) fused level
 #define TP_TRACE_DECL long long tp_tr[12]
 #define TP_TRACE(k) tp_tr[k] = clock64()
 #define TP_TRACE_FLUSH \
     do { if (threadIdx.x == 0) for (int k_ = 0; k_ < 12; ++k_) g_trace[k_] = tp_tr[k_]; } while (0)
+#define TP_LF_TRACE(k) do { if (threadIdx.x == 0 && blockIdx.x == 0) g_trace[12 + (k)] = clock64(); } while (0)
 #else
+#define TP_LF_TRACE(k) do { } while (0)
 #define TP_TRACE_DECL
 #define TP_TRACE(k) do { } while (0)
 #define TP_TRACE_FLUSH do { } while (0)
@@ -322,6 +324,32 @@ cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const Iface
                     link != nullptr ? *link : none);
 }
 
+// k_level_final_cl: odd block stride, >= m + 1 (the tail block has <= m + 1 rows)
+static int level_final_stride(int64_t m) { return (int)((m + 1) % 2 == 1 ? m + 1 : m + 2); }
+constexpr size_t kLfDynSmem = 176 * 1024;  // + 40 KB static (interface rows, solution)
+static bool g_fuse_last = true;
+
+static size_t level_final_smem(int64_t m, int64_t K, size_t elem) {
+    return (size_t)4 * (size_t)((K + kFinCS - 1) / kFinCS) * (size_t)level_final_stride(m) * elem;
+}
+
+bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem) {
+    if (!g_fuse_last || !g_final_cluster || m < 4 || m > 4096 || K < kFinClusterMin) return false;
+    if ((K + kFinCS - 1) / kFinCS > kLfMaxBlocks || 2 * K > kFinalCap) return false;
+    if ((K - 1) * m >= n || n - (K - 1) * m > m + 1) return false;  // make_plan's shape
+    return level_final_smem(m, K, elem) <= kLfDynSmem;
+}
+
+template <class T>
+cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, T* x,
+                               unsigned long long* err, int level, cudaStream_t st) {
+    if (!level_final_fits(n, m, K, sizeof(T))) return cudaErrorInvalidValue;
+    auto k = m == 4 ? k_level_final_cl<T, 4> : m == 8 ? k_level_final_cl<T, 8>
+             : m == 16 ? k_level_final_cl<T, 16> : k_level_final_cl<T, 0>;
+    return launch_k(level, k, kFinCS, kFinNT, level_final_smem(m, K, sizeof(T)), st, sys, n, (int)m, K,
+                    level_final_stride(m), x, err, level);
+}
+
 template <class T>
 static cudaError_t set_smem_attributes() {
     const int fs = (int)(kMaxDynSmem - 4096);
@@ -332,12 +360,15 @@ static cudaError_t set_smem_attributes() {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kShard>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
+    for (auto k : {k_level_final_cl<T, 0>, k_level_final_cl<T, 4>, k_level_final_cl<T, 8>, k_level_final_cl<T, 16>})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLfDynSmem);
     return e;
 }
 
 cudaError_t init_kernel_attributes() {
     if (const char* v = getenv("TPB_PDL")) g_pdl = atoi(v);
     if (const char* v = getenv("TPB_FINAL_CLUSTER")) g_final_cluster = atoi(v) != 0;
+    if (const char* v = getenv("TPB_FUSE_LAST")) g_fuse_last = atoi(v) != 0;
     cudaError_t e = set_smem_attributes<double>();
     if (e == cudaSuccess) e = set_smem_attributes<float>();
     return e;
@@ -383,6 +414,8 @@ cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsign
     template cudaError_t launch_final<T>(int, const SysPtrs<T>&, int64_t, const IfacePtrs<T>&,      \
                                          const T*, T*, unsigned long long*, int, cudaStream_t,      \
                                          const ShardLink*);                                         \
+    template cudaError_t launch_level_final<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t, T*,    \
+                                               unsigned long long*, int, cudaStream_t);             \
     template cudaError_t launch_gather_solve<T>(const T*, int, int, T*, T*, unsigned long long*,    \
                                                 int, cudaStream_t);                                 \
     template cudaError_t launch_generate<T>(int64_t, int64_t, int64_t, uint64_t, double, T*, T*,    \

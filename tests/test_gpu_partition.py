@@ -442,3 +442,38 @@ def test_randomized_large_sizes_and_deep_policies(tp, oracle_mod):
         s = oracle_mod.generate_system(n, 50_000 + case)
         _check(oracle_mod, s, tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes)),
                oracle_mod.solve_partition(s, sizes))
+
+
+@pytest.mark.parametrize(
+    "n,sizes",
+    [
+        (10_000, [4]),          # C1: the whole solve is one cluster kernel
+        (4_097, [64]),          # K = 64, the smallest fused level
+        (20_000, [16]),         # tail of 16 rows (== m) and short tails below
+        (20_001, [16]),         # tail of m + 1 rows
+        (20_007, [16]),         # short tail
+        (30_000, [255]),        # odd m, stride m + 2
+        (1_000_000, [64, 10]),  # deepest of two levels fused
+        (250_003, [8, 7]),      # odd m at the fused level, ragged
+    ],
+)
+def test_fused_deepest_level(tp, oracle_mod, n, sizes):
+    """k_level_final_cl (deepest level + finishing solve in one cluster
+    kernel) against the oracle, across stride / tail shapes."""
+    s = oracle_mod.generate_system(n, 23)
+    x = tp.solve_partition(tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs), tp.RecursionPolicy(sizes))
+    _check(oracle_mod, s, x, oracle_mod.solve_partition(s, sizes))
+
+
+def test_fused_deepest_level_reports_zero_pivots(tp):
+    """A zero row inside the fused level (its block sweeps) and one that only
+    breaks the interface solve both surface as ZeroPivotError."""
+    n = 20_000
+    sub, diag, sup, rhs = np.zeros(n), np.ones(n), np.zeros(n), np.ones(n)
+    for row in (5, 16, 7_777, n - 1):
+        d = diag.copy()
+        d[row] = 0.0
+        with pytest.raises(tp.ZeroPivotError):
+            tp.solve_partition(tp.TridiagonalSystem(sub, d, sup, rhs), tp.RecursionPolicy([16]))
+    x = tp.solve_partition(tp.TridiagonalSystem(sub, diag, sup, rhs), tp.RecursionPolicy([16]))
+    assert np.allclose(x, 1.0)

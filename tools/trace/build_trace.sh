@@ -1,8 +1,10 @@
 #!/bin/bash
-# scratch build of the library with k_final phase tracing (-DTPB_TRACE)
+# scratch build of the library with finishing-solve phase tracing (-DTPB_TRACE);
+# extra nvcc flags (e.g. -DTPB_LF_STAGE=1) and TRACE_OUT (output dir) are optional
 set -e
-cd "$(dirname "$0")"; mkdir -p ../../scratch/trace_lib
-
+cd "$(dirname "$0")"
+OUT=${TRACE_OUT:-../../scratch/trace_lib}; mkdir -p $OUT
 C=../../paper_2510_27351_b200/csrc
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -DTPB_TRACE -c $C/tp_kernels.cu -o ../../scratch/trace_lib/tp_kernels.o
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../scratch/trace_lib/libtridpart_b200.so ../../scratch/trace_lib/tp_kernels.o ../../paper_2510_27351_b200/lib/tp_capi.o ../../paper_2510_27351_b200/lib/tp_knn.o -cudart static
+L=../../paper_2510_27351_b200/lib
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -DTPB_TRACE "$@" -c $C/tp_kernels.cu -o $OUT/tp_kernels.o
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libtridpart_b200.so $OUT/tp_kernels.o $L/tp_capi.o $L/tp_knn.o $L/tp_stage.o -cudart static
