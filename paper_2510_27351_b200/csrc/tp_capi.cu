@@ -309,7 +309,7 @@ struct Runner {
     }
     // The deepest level and the finishing solve run as one cluster kernel when
     // that level fits the cluster's shared memory (k_level_final_cl); its
-    // interface system and solution then never touch HBM.
+    // interface is still written out (for the observer), never read back.
     void solve_body(const Plan<T>& p) {
         const size_t nl = p.levels.size();
         const bool fuse = nl > 0 && tpb::level_final_fits(p.levels.back().n, p.levels.back().m,
@@ -318,7 +318,7 @@ struct Runner {
         for (size_t l = 0; l < top; ++l) stage(p.levels[l], (int)l, tpb::kStage1);
         if (fuse) {
             const Level<T>& L = p.levels.back();
-            check(tpb::launch_level_final<T>(L.in, L.n, L.m, L.K, L.x_out, ctx->d_err, (int)top, st));
+            check(tpb::launch_level_final<T>(L.in, L.n, L.m, L.K, L.iface, L.x_out, ctx->d_err, (int)top, st));
             after("level_final", (int)top);
         } else {
             final_solve(p);

@@ -321,7 +321,7 @@ constexpr int kFinRows = kFinNT * 4;  // rows staged per CTA (chunks <= 4 rows)
 // the chunking is local to the CTA (its first rows % per chunks get the extra
 // row), which equals k_final_cl's global chunking when every CTA owns the same
 // number of chunks. The solution rows go to xdst[row - xbase].
-template <class T, int MODE, class CtaRow0>
+template <class T, int MODE, int CS = kFinCS, class CtaRow0>
 __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, const T* sa, const T* sb,
                                         const T* sc, const T* sd, int64_t r0, int rows, int per,
                                         CtaRow0 cta_row0, int64_t n, const IfacePtrs<T>& out,
@@ -398,13 +398,14 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
     // ---- CTA 0, warp 0: the CTA roots (3 levels), the root, and back down ----
     if (cta == 0 && warp == 0) {
         Eq2<T> cc = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
-        if (lane < kFinCS) cc = *cl.map_shared_rank(&croot, lane);
-        MergeSave<T> sc3[3];
+        if (lane < CS) cc = *cl.map_shared_rank(&croot, lane);
+        constexpr int kCLv = CS == 16 ? 4 : 3;  // levels over the CTA roots
+        MergeSave<T> sc3[kCLv];
 #pragma unroll
-        for (int lv = 0; lv < 3; ++lv) {
+        for (int lv = 0; lv < kCLv; ++lv) {
             const int h = 1 << lv;
             const Eq2<T> oth = shfl_down_eq(cc, h);
-            if ((lane & (2 * h - 1)) == 0 && lane + h < kFinCS)
+            if ((lane & (2 * h - 1)) == 0 && lane + h < CS)
                 cc = merge(cc, oth, cta_row0(lane + h) - 1, bad, sc3[lv]);
         }
         T xs = 0, xe = 0;
@@ -432,7 +433,7 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
         }
         if constexpr (MODE != kStage1) {
 #pragma unroll
-            for (int lv = 2; lv >= 0; --lv) {
+            for (int lv = kCLv - 1; lv >= 0; --lv) {
                 const int h = 1 << lv;
                 T xt = 0;
                 if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sc3[lv], xs, xe);
@@ -445,7 +446,7 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
                     xe = xt;
                 }
             }
-            if (lane < kFinCS) {
+            if (lane < CS) {
                 T* dst = cl.map_shared_rank(&cx[0], lane);
                 dst[0] = xs;
                 dst[1] = xe;
@@ -575,7 +576,8 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
 // thread sweeps one block at a time (leaf_smem, partition.hpp:90-124, the same
 // arithmetic as k_generic with one lane per block), the block's E1/E2 rows are
 // this CTA's rows of the interface (assemble_interface order,
-// partition.hpp:139-149), cl_tree solves the interface across the cluster,
+// partition.hpp:139-149; also stored to HBM for the observer), cl_tree solves
+// the interface across the cluster,
 // and each thread back-substitutes its block from the kept sweep values
 // (partition.hpp:154-173) before one coalesced store. The interface never
 // leaves the SMs. Blocks are padded to an odd stride S >= m + 1 so the
@@ -631,9 +633,11 @@ __device__ __forceinline__ void lf_expand_regs(T* a, const T* rbp, const T* gp, 
 }
 
 // MF = m when m is 4, 8 or 16 (register sweeps for the full blocks), else 0.
-template <class T, int MF>
-__global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
-    k_level_final_cl(SysPtrs<T> sys, int64_t n, int m, int64_t K, int S, T* __restrict__ x,
+// CS = CTAs per cluster (8, or 16 where the GPU can co-schedule a
+// non-portable 16-CTA cluster); the cluster shape is set at launch.
+template <class T, int MF, int CS>
+__global__ void __launch_bounds__(kFinNT, 1)
+    k_level_final_cl(SysPtrs<T> sys, int64_t n, int m, int64_t K, int S, IfacePtrs<T> iface, T* __restrict__ x,
                      unsigned long long* err, int level) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
@@ -641,9 +645,9 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
     __shared__ T fa[kFinRows], fb[kFinRows], fc[kFinRows], fd[kFinRows], fx[kFinRows];
     const int tid = threadIdx.x;
     const int cta = (int)cl.block_rank();
-    const int64_t B0 = K * cta / kFinCS, B1 = K * (cta + 1) / kFinCS;
+    const int64_t B0 = K * cta / CS, B1 = K * (cta + 1) / CS;
     const int nb = (int)(B1 - B0);
-    const int nbmax = (int)((K + kFinCS - 1) / kFinCS);
+    const int nbmax = (int)((K + CS - 1) / CS);
     T* la = reinterpret_cast<T*>(lf_raw);
     T* lb = la + (size_t)nbmax * S;
     T* lc = lb + (size_t)nbmax * S;
@@ -691,14 +695,22 @@ __global__ void __cluster_dims__(kFinCS, 1, 1) __launch_bounds__(kFinNT, 1)
         fd[2 * jj] = q.d1; fd[2 * jj + 1] = q.d2;
     }
     __syncthreads();
+    // the interface also goes to HBM (2 rows per block, coalesced, off the
+    // critical path): the observer overload reports every level's interface
+    for (int i = tid; i < 2 * nb; i += kFinNT) {
+        iface.sub[2 * B0 + i] = fa[i];
+        iface.diag[2 * B0 + i] = fb[i];
+        iface.sup[2 * B0 + i] = fc[i];
+        iface.rhs[2 * B0 + i] = fd[i];
+    }
     TP_LF_TRACE(2);
 
     // ---- the interface (2K rows) across the cluster ----
     int per = 1;
     while (per * 2 <= kFinNT && per * 2 <= nb) per *= 2;
     const ShardLink none{};
-    cl_tree<T, kSolve>(cl, fa, fb, fc, fd, 2 * B0, 2 * nb, per,
-                       [&](int c) { return 2 * (K * c / kFinCS); }, 2 * K, IfacePtrs<T>{}, nullptr, fx,
+    cl_tree<T, kSolve, CS>(cl, fa, fb, fc, fd, 2 * B0, 2 * nb, per,
+                       [&](int c) { return 2 * (K * c / CS); }, 2 * K, IfacePtrs<T>{}, nullptr, fx,
                        2 * B0, bad_fin, err, level + 1, none);
     __syncthreads();
     TP_LF_TRACE(3);

@@ -125,19 +125,35 @@ __global__ void k_residual(SysPtrs<T> sys, int64_t n, const T* __restrict__ x, u
 static int g_pdl = 0;
 
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_k(int level, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
-                            cudaStream_t st, Args... args) {
+static cudaError_t launch_kc(int level, unsigned cluster, void (*kern)(KArgs...), unsigned grid, unsigned block,
+                             size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (g_pdl == 1 || (g_pdl == 2 && level > 0)) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster > 0) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = cluster;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = (g_pdl == 1 || (g_pdl == 2 && level > 0)) ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+template <class... KArgs, class... Args>
+static cudaError_t launch_k(int level, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                            cudaStream_t st, Args... args) {
+    return launch_kc(level, 0, kern, grid, block, smem, st, args...);
 }
 
 // Error-word reset at the head of every solve (a kernel rather than a memset
@@ -328,26 +344,74 @@ cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const Iface
 static int level_final_stride(int64_t m) { return (int)((m + 1) % 2 == 1 ? m + 1 : m + 2); }
 constexpr size_t kLfDynSmem = 176 * 1024;  // + 40 KB static (interface rows, solution)
 static bool g_fuse_last = true;
+// CTAs per cluster of the fused kernel: 16 (non-portable) when the GPU can
+// co-schedule it, else 8; TPB_LF_CLUSTER=8 forces the portable shape
+static int g_lf_cs = 8;
 
 static size_t level_final_smem(int64_t m, int64_t K, size_t elem) {
-    return (size_t)4 * (size_t)((K + kFinCS - 1) / kFinCS) * (size_t)level_final_stride(m) * elem;
+    return (size_t)4 * (size_t)((K + g_lf_cs - 1) / g_lf_cs) * (size_t)level_final_stride(m) * elem;
 }
 
 bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem) {
-    if (!g_fuse_last || !g_final_cluster || m < 4 || m > 4096 || K < kFinClusterMin) return false;
-    if ((K + kFinCS - 1) / kFinCS > kLfMaxBlocks || 2 * K > kFinalCap) return false;
+    // m <= 16: above that the one-thread-per-block sweeps of the fused kernel
+    // lose to the level kernels' lane trees (C2, m = 32: 24.7 vs 22.6 us per solve)
+    if (!g_fuse_last || !g_final_cluster || m < 4 || m > 16 || K < kFinClusterMin) return false;
+    if ((K + g_lf_cs - 1) / g_lf_cs > kLfMaxBlocks || 2 * K > kFinalCap) return false;
     if ((K - 1) * m >= n || n - (K - 1) * m > m + 1) return false;  // make_plan's shape
     return level_final_smem(m, K, elem) <= kLfDynSmem;
 }
 
+template <class T, int CS>
+static void (*level_final_kernel(int64_t m))(SysPtrs<T>, int64_t, int, int64_t, int, IfacePtrs<T>, T*,
+                                              unsigned long long*, int) {
+    return m == 4 ? k_level_final_cl<T, 4, CS> : m == 8 ? k_level_final_cl<T, 8, CS>
+           : m == 16 ? k_level_final_cl<T, 16, CS> : k_level_final_cl<T, 0, CS>;
+}
+
 template <class T>
-cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, T* x,
-                               unsigned long long* err, int level, cudaStream_t st) {
+cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, const IfacePtrs<T>& iface,
+                               T* x, unsigned long long* err, int level, cudaStream_t st) {
     if (!level_final_fits(n, m, K, sizeof(T))) return cudaErrorInvalidValue;
-    auto k = m == 4 ? k_level_final_cl<T, 4> : m == 8 ? k_level_final_cl<T, 8>
-             : m == 16 ? k_level_final_cl<T, 16> : k_level_final_cl<T, 0>;
-    return launch_k(level, k, kFinCS, kFinNT, level_final_smem(m, K, sizeof(T)), st, sys, n, (int)m, K,
-                    level_final_stride(m), x, err, level);
+    auto k = g_lf_cs == 16 ? level_final_kernel<T, 16>(m) : level_final_kernel<T, 8>(m);
+    return launch_kc(level, (unsigned)g_lf_cs, k, (unsigned)g_lf_cs, kFinNT, level_final_smem(m, K, sizeof(T)), st,
+                     sys, n, (int)m, K, level_final_stride(m), iface, x, err, level);
+}
+
+template <class T, int CS>
+static cudaError_t set_level_final_attributes() {
+    cudaError_t e = cudaSuccess;
+    for (int64_t m : {4, 8, 16, 0}) {
+        auto k = level_final_kernel<T, CS>(m);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLfDynSmem);
+        if (e == cudaSuccess && CS > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+    return e;
+}
+
+// 16 when a 16-CTA cluster of the fused kernel at full shared memory fits the GPU
+static int probe_level_final_cluster() {
+    if (set_level_final_attributes<double, 16>() != cudaSuccess ||
+        set_level_final_attributes<float, 16>() != cudaSuccess) {
+        cudaGetLastError();
+        return 8;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(kFinNT);
+    cfg.dynamicSmemBytes = kLfDynSmem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 16;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)k_level_final_cl<double, 16, 16>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 8;
+    }
+    return nclusters >= 1 ? 16 : 8;
 }
 
 template <class T>
@@ -360,8 +424,7 @@ static cudaError_t set_smem_attributes() {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kStage3>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kSolve>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_final<T, kShard>, cudaFuncAttributeMaxDynamicSharedMemorySize, fs);
-    for (auto k : {k_level_final_cl<T, 0>, k_level_final_cl<T, 4>, k_level_final_cl<T, 8>, k_level_final_cl<T, 16>})
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLfDynSmem);
+    if (e == cudaSuccess) e = set_level_final_attributes<T, 8>();
     return e;
 }
 
@@ -371,6 +434,8 @@ cudaError_t init_kernel_attributes() {
     if (const char* v = getenv("TPB_FUSE_LAST")) g_fuse_last = atoi(v) != 0;
     cudaError_t e = set_smem_attributes<double>();
     if (e == cudaSuccess) e = set_smem_attributes<float>();
+    g_lf_cs = probe_level_final_cluster();
+    if (const char* v = getenv("TPB_LF_CLUSTER")) if (atoi(v) == 8) g_lf_cs = 8;
     return e;
 }
 
@@ -414,7 +479,8 @@ cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsign
     template cudaError_t launch_final<T>(int, const SysPtrs<T>&, int64_t, const IfacePtrs<T>&,      \
                                          const T*, T*, unsigned long long*, int, cudaStream_t,      \
                                          const ShardLink*);                                         \
-    template cudaError_t launch_level_final<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t, T*,    \
+    template cudaError_t launch_level_final<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t,        \
+                                               const IfacePtrs<T>&, T*,                             \
                                                unsigned long long*, int, cudaStream_t);             \
     template cudaError_t launch_gather_solve<T>(const T*, int, int, T*, T*, unsigned long long*,    \
                                                 int, cudaStream_t);                                 \

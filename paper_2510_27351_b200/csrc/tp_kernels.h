@@ -86,8 +86,8 @@ cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const Iface
 // when it does not (the caller then runs the three-kernel form).
 bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem);
 template <class T>
-cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, T* x,
-                               unsigned long long* err, int level, cudaStream_t st);
+cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, const IfacePtrs<T>& iface,
+                               T* x, unsigned long long* err, int level, cudaStream_t st);
 template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st);

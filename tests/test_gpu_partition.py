@@ -452,7 +452,7 @@ def test_randomized_large_sizes_and_deep_policies(tp, oracle_mod):
         (20_000, [16]),         # tail of 16 rows (== m) and short tails below
         (20_001, [16]),         # tail of m + 1 rows
         (20_007, [16]),         # short tail
-        (30_000, [255]),        # odd m, stride m + 2
+        (30_000, [13]),         # odd m, stride m + 2
         (1_000_000, [64, 10]),  # deepest of two levels fused
         (250_003, [8, 7]),      # odd m at the fused level, ragged
     ],
