@@ -54,10 +54,11 @@ def main():
                 kind = "kernel"
             evs.append((e.time_range.start, e.time_range.end, nm, kind))
     evs.sort()
-    # split into replays at gaps > 50 us
+    # split into replays: every solve graph starts with k_reset (fall back to
+    # gaps > 50 us for graphs without it)
     groups, cur = [], []
     for ev in evs:
-        if cur and ev[0] - max(c[1] for c in cur) > 50:
+        if cur and ("k_reset" in ev[2] or ev[0] - max(c[1] for c in cur) > 50):
             groups.append(cur)
             cur = []
         cur.append(ev)
