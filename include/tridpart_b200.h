@@ -204,8 +204,11 @@ tp_status tp_generate_system_f32_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64
 /* make_plan(n, m) — partition.hpp:30-49. bounds (optional) gets K+1 entries. */
 tp_status tp_make_plan(int64_t n, int64_t m, int64_t* bounds, int64_t* nblocks, tp_error* err);
 
-/* Level structure the device solve will execute: per level its size and m;
- * n_final is the size of the system handed to the finishing solver. */
+/* Level structure the device solve will execute: per level its size and m
+ * (negative m = device-internal level); n_final is the size of the system
+ * handed to the finishing solver. When the deepest level runs fused with the
+ * finishing solve (k_level_final_cl; needs m <= 16 and a CUDA context, whose
+ * creation fixes the cluster shape) n_final may exceed 6144. */
 tp_status tp_plan_levels(int64_t n, const int64_t* sizes, int32_t nsizes, int64_t* level_n,
                          int64_t* level_m, int32_t* nlevels, int32_t max_levels, int64_t* n_final,
                          tp_error* err);

@@ -31,6 +31,7 @@ using tpb::SysPtrs;
 namespace {
 
 constexpr int64_t kInternalM = 32;
+constexpr int64_t kFusedInternalM = 16;  // internal level absorbed by k_level_final_cl
 
 void set_err(tp_error* err, tp_status code, const std::string& msg, int64_t row = -1, int32_t level = -1) {
     if (!err) return;
@@ -98,8 +99,13 @@ struct Plan {
 
 inline size_t pad32(size_t v) { return (v + 31) & ~size_t(31); }
 
+// fused = the plan is for solve_body, which runs the deepest level and the
+// finishing solve as one kernel when that level fits k_level_final_cl: then
+// the deepest interface may exceed kFinalCap (no device-internal level is
+// added for it), and an oversized final system gets ONE fused internal level
+// of m = 16 when that fits. The sharded paths keep n_final <= kFinalCap.
 template <class T>
-void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p) {
+void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p, bool fused = false) {
     p.levels.clear();
     int64_t cur = n;
     int lvl = 0;
@@ -127,11 +133,15 @@ void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p) {
         if (lvl == nsizes - 1) break;
         ++lvl;
     }
-    // device-internal levels so the finishing solve fits one CTA
-    while (cur > tpb::kFinalCap) {
+    // device-internal levels so the finishing solve fits one cluster
+    const bool last_fused = fused && !p.levels.empty() &&
+                            tpb::level_final_fits(p.levels.back().n, p.levels.back().m, p.levels.back().K, sizeof(T));
+    while (!last_fused && cur > tpb::kFinalCap) {
         Level<T> L;
         L.n = cur;
         L.m = kInternalM;
+        if (fused && tpb::level_final_fits(cur, kFusedInternalM, plan_blocks(cur, kFusedInternalM), sizeof(T)))
+            L.m = kFusedInternalM;
         L.K = plan_blocks(cur, L.m);
         const int64_t last_len = cur - (L.K - 1) * L.m;
         L.kfull = (last_len == L.m) ? L.K : L.K - 1;
@@ -140,6 +150,7 @@ void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p) {
         ws += 5 * pad32((size_t)(2 * L.K));
         p.levels.push_back(L);
         cur = 2 * L.K;
+        if (L.m == kFusedInternalM) break;  // solved by k_level_final_cl
     }
     p.n_final = cur;
     p.ws_elems = ws;
@@ -538,7 +549,7 @@ tp_status solve_dev(tp_ctx* ctx, const T* sub, const T* diag, const T* super, co
     if (s != TP_OK) return s;
     TP_CUDA(cudaSetDevice(ctx->device));
     Plan<T> p;
-    build_plan(n, sizes, nsizes, p);
+    build_plan(n, sizes, nsizes, p, true);
     s = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
     if (s != TP_OK) return s;
     bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, x, ctx->ws);
@@ -630,7 +641,7 @@ tp_status solve_observe(tp_ctx* ctx, const T* sub, const T* diag, const T* super
     s = ensure_dsys<T>(ctx, n, d, err);  // same buffers the solve used
     if (s != TP_OK) return s;
     Plan<T> p;
-    build_plan(n, sizes, nsizes, p);
+    build_plan(n, sizes, nsizes, p, true);
     bind_plan(p, SysPtrs<T>{d[0], d[1], d[2], d[3]}, d[4], ctx->ws);
     std::vector<T> h;
     for (size_t l = 0; l < p.levels.size(); ++l) {
@@ -666,7 +677,7 @@ tp_status thomas_host(tp_ctx* ctx, const T* sub, const T* diag, const T* super, 
         ctx, sub, diag, super, rhs, n, x,
         [&](T** d, cudaStream_t st) -> tp_status {
             Plan<T> p;
-            build_plan(n, nullptr, 0, p);
+            build_plan(n, nullptr, 0, p, true);
             tp_status s2 = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
             if (s2 != TP_OK) return s2;
             bind_plan(p, SysPtrs<T>{d[0], d[1], d[2], d[3]}, d[4], ctx->ws);
@@ -1156,7 +1167,7 @@ tp_status tp_plan_levels(int64_t n, const int64_t* sizes, int32_t nsizes, int64_
     tp_status s = validate_policy(n, sizes, nsizes, err);
     if (s != TP_OK) return s;
     Plan<double> p;
-    build_plan(n, sizes, nsizes, p);
+    build_plan(n, sizes, nsizes, p, true);
     if ((int32_t)p.levels.size() > max_levels) {
         set_err(err, TP_ERR_INVALID_ARGUMENT, "max_levels too small");
         return TP_ERR_INVALID_ARGUMENT;
@@ -1182,7 +1193,7 @@ tp_status tp_solve_profile_f64_dev(tp_ctx* ctx, const double* sub, const double*
     if (s != TP_OK) return s;
     TP_CUDA(cudaSetDevice(ctx->device));
     Plan<double> p;
-    build_plan(n, sizes, nsizes, p);
+    build_plan(n, sizes, nsizes, p, true);
     s = ensure_ws(ctx, p.ws_elems * sizeof(double), err);
     if (s != TP_OK) return s;
     bind_plan(p, SysPtrs<double>{sub, diag, super, rhs}, x, ctx->ws);

@@ -354,9 +354,10 @@ static size_t level_final_smem(int64_t m, int64_t K, size_t elem) {
 
 bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem) {
     // m <= 16: above that the one-thread-per-block sweeps of the fused kernel
-    // lose to the level kernels' lane trees (C2, m = 32: 24.7 vs 22.6 us per solve)
+    // lose to the level kernels' lane trees (C2, m = 32: 24.7 vs 22.6 us per solve).
+    // The interface may exceed kFinalCap: each CTA solves <= 2 * kLfMaxBlocks of it.
     if (!g_fuse_last || !g_final_cluster || m < 4 || m > 16 || K < kFinClusterMin) return false;
-    if ((K + g_lf_cs - 1) / g_lf_cs > kLfMaxBlocks || 2 * K > kFinalCap) return false;
+    if ((K + g_lf_cs - 1) / g_lf_cs > kLfMaxBlocks) return false;
     if ((K - 1) * m >= n || n - (K - 1) * m > m + 1) return false;  // make_plan's shape
     return level_final_smem(m, K, elem) <= kLfDynSmem;
 }

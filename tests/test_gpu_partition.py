@@ -455,6 +455,9 @@ def test_randomized_large_sizes_and_deep_policies(tp, oracle_mod):
         (30_000, [13]),         # odd m, stride m + 2
         (1_000_000, [64, 10]),  # deepest of two levels fused
         (250_003, [8, 7]),      # odd m at the fused level, ragged
+        (60_000, [8]),          # 15,000-row interface (> 6144) solved on the 16-CTA cluster
+        (1_000_000, [32]),      # C2: fused device-internal level (m = 16)
+        (2_000_003, [64]),      # fused device-internal level with a tail
     ],
 )
 def test_fused_deepest_level(tp, oracle_mod, n, sizes):
@@ -477,3 +480,17 @@ def test_fused_deepest_level_reports_zero_pivots(tp):
             tp.solve_partition(tp.TridiagonalSystem(sub, d, sup, rhs), tp.RecursionPolicy([16]))
     x = tp.solve_partition(tp.TridiagonalSystem(sub, diag, sup, rhs), tp.RecursionPolicy([16]))
     assert np.allclose(x, 1.0)
+
+
+def test_plan_uses_the_fused_internal_level(tp):
+    """With a context (16-CTA cluster probed), C2's oversized interface gets
+    one m = 16 internal level that the fused kernel absorbs."""
+    import torch
+
+    tp.generate_system(1000, 1, device=True)  # creates the context
+    torch.cuda.synchronize()
+    ln, lm, nf = tp.plan_levels(1_000_000, [32])
+    assert ln[0] == 1_000_000 and lm[0] == 32
+    assert lm[-1] in (-16, -32)
+    if lm[-1] == -16:
+        assert ln == [1_000_000, 62_500] and nf == 7_814  # make_plan(62500, 16): 3907 blocks
