@@ -494,3 +494,38 @@ def test_plan_uses_the_fused_internal_level(tp):
     assert lm[-1] in (-16, -32)
     if lm[-1] == -16:
         assert ln == [1_000_000, 62_500] and nf == 7_814  # make_plan(62500, 16): 3907 blocks
+
+
+def test_fused_deepest_level_random_shapes(tp, oracle_mod):
+    """200 random solves whose deepest level goes through k_level_final_cl:
+    last-level m in [4, 16] (register and shared-memory sweeps), K from 64 to
+    ~8000 blocks (interfaces above the 6144-row cap of the plain finishing
+    solve), every tail length, FP64 against the oracle (all three gates) and
+    every 4th case also in FP32 (1e-4)."""
+    rng = np.random.default_rng(515)
+    fused = 0
+    for case in range(200):
+        m_last = int(rng.integers(4, 17))
+        k_last = int(np.exp(rng.uniform(np.log(64), np.log(7_900))))
+        n_last = k_last * m_last + int(rng.integers(0, m_last))
+        depth = int(rng.integers(0, 3))
+        # lead levels that shrink to ~n_last rows: N = n_last * m0 / 2 * ...
+        sizes = [m_last]
+        n = n_last
+        for _ in range(depth):
+            m0 = int(rng.integers(4, 65))
+            sizes.insert(0, m0)
+            n = n * m0 // 2 + int(rng.integers(0, m0))
+        if n > 3_000_000:  # keep the oracle quick
+            sizes, n = [m_last], n_last
+        ln, lm, _ = tp.plan_levels(n, sizes)
+        fused += int(lm[-1] > 0 and lm[-1] <= 16 and ln[-1] >= 64 * lm[-1])
+        s = oracle_mod.generate_system(n, 7_000 + case)
+        ref = oracle_mod.solve_partition(s, sizes)
+        _check(oracle_mod, s, tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes)), ref)
+        if case % 4 == 0:
+            x32 = tp.solve_partition(
+                tp.TridiagonalSystem(*(a.astype(np.float32) for a in (s.sub, s.diag, s.sup, s.rhs))),
+                tp.RecursionPolicy(sizes))
+            assert oracle_mod.rel_inf_diff(x32.astype(np.float64), ref) <= 1e-4, (case, n, sizes)
+    assert fused >= 150  # most cases really take the fused kernel
