@@ -326,7 +326,19 @@ struct Runner {
         const bool fuse = nl > 0 && tpb::level_final_fits(p.levels.back().n, p.levels.back().m,
                                                           p.levels.back().K, sizeof(T));
         const size_t top = fuse ? nl - 1 : nl;
-        for (size_t l = 0; l < top; ++l) stage(p.levels[l], (int)l, tpb::kStage1);
+        size_t l = 0;
+        if (top >= 2) {  // level 1's Stage 1 folded into level 0's (k_fast_s1fold)
+            const Level<T>& A = p.levels[0];
+            const Level<T>& B = p.levels[1];
+            if (A.tail == 0 && A.kfull == A.K && B.tail == 0 && tpb::fold_fits(A.m, A.K, B.n, B.m, B.K)) {
+                const bool vec = aligned32(A.in.sub) && aligned32(A.in.diag) && aligned32(A.in.sup) &&
+                                 aligned32(A.in.rhs);
+                check(tpb::launch_fold<T>(A.m, vec, A.in, A.K, A.iface, B.m, B.K, B.iface, ctx->d_err, 0, st));
+                after("stage1_fold", 0);
+                l = 2;
+            }
+        }
+        for (; l < top; ++l) stage(p.levels[l], (int)l, tpb::kStage1);
         if (fuse) {
             const Level<T>& L = p.levels.back();
             check(tpb::launch_level_final<T>(L.in, L.n, L.m, L.K, L.iface, L.x_out, ctx->d_err, (int)top, st));

@@ -1,0 +1,81 @@
+// Stage 1 of level 0 with level 1's Stage 1 folded in (k_fast_s1fold).
+//
+// When level 1's block size m1 is even, one level-1 block is exactly h = m1/2
+// level-0 blocks' interface rows (assemble_interface order, partition.hpp:
+// 139-149). A CTA here owns 16 level-1 blocks = 16 h level-0 blocks: it runs
+// the k_fast Stage-1 pass over them h times (16 level-0 blocks per pass, G
+// lanes each), keeps their E1/E2 rows in shared memory as well as writing
+// them to HBM (Stage 3 of level 1 reads that system), then 16 threads sweep
+// the 16 level-1 blocks from shared memory (leaf_smem, partition.hpp:90-124)
+// and write level 2's system. The separate Stage-1 kernel of level 1 and its
+// 100 MB re-read (C3) disappear.
+#pragma once
+#include "tp_fast.cuh"
+#include "tp_generic.cuh"
+
+namespace tpb {
+
+constexpr int kFoldL1Blocks = 16;  // level-1 blocks per CTA
+
+template <class T, int L, int G, bool VEC, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    k_fast_s1fold(SysPtrs<T> sys, int64_t nblocks0, IfacePtrs<T> out0, int m1, int64_t nblocks1,
+                  IfacePtrs<T> out1, unsigned long long* err, int level) {
+    static_assert(32 % G == 0, "G must divide the warp");
+    constexpr int BP = THREADS / G;  // level-0 blocks per pass
+    static_assert(BP == kFoldL1Blocks, "one pass = 16 level-0 blocks");
+    extern __shared__ __align__(16) unsigned char fold_raw[];
+    const int h = m1 / 2;                           // level-0 blocks per level-1 block
+    const int rows1 = kFoldL1Blocks * m1;           // level-1 rows per CTA
+    T* sa = reinterpret_cast<T*>(fold_raw);
+    T* sb = sa + rows1;
+    T* sc = sb + rows1;
+    T* sd = sc + rows1;
+    const int c = (threadIdx.x & 31) % G;
+    const int64_t blk0_base = (int64_t)blockIdx.x * kFoldL1Blocks * h;
+    pdl_begin();
+
+    for (int p = 0; p < h; ++p) {
+        const int lb = p * BP + (int)threadIdx.x / G;  // level-0 block inside the tile
+        const int64_t blk = blk0_base + lb;
+        const bool active = blk < nblocks0;           // warp-uniform (BP blocks per pass, G | 32)
+        const int64_t t = blk * G + c;
+        const int64_t row0 = t * L;
+        LaneState<T, L, G, false> s;
+        load_chunk<T, L, VEC>(sys, row0, active, s.r);
+        lane_leaf<T, L, G, false>(s, row0);
+        lanes_tree<T, L, G, false>(s, c, row0);
+        if (active) {
+            if (s.guard.tripped()) report_pivot(err, level, row0);
+            if (c == 0) {
+                store_block_eqs(out0, blk, s.cur);
+                const int r = 2 * lb;
+                sa[r] = s.cur.a1; sa[r + 1] = s.cur.a2;
+                sb[r] = s.cur.b1; sb[r + 1] = s.cur.b2;
+                sc[r] = s.cur.g1; sc[r + 1] = s.cur.g2;
+                sd[r] = s.cur.d1; sd[r + 1] = s.cur.d2;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < kFoldL1Blocks) {
+        const int64_t j = (int64_t)blockIdx.x * kFoldL1Blocks + threadIdx.x;
+        if (j < nblocks1) {
+            const int o = (int)threadIdx.x * m1;
+            RowGuard bad;
+            Eq2<T> q;
+            if (m1 == 10) {  // C3's level 1: both sweeps from registers (independent chains)
+                Chunk<T, 10> r;
+#pragma unroll
+                for (int i = 0; i < 10; ++i) { r.a[i] = sa[o + i]; r.b[i] = sb[o + i]; r.c[i] = sc[o + i]; r.d[i] = sd[o + i]; }
+                q = leaf_reduce<T, 10, 10>(r, j * m1, bad);
+            } else {
+                q = leaf_smem<T, false>(sa + o, sb + o, sc + o, sd + o, m1, j * m1, bad);
+            }
+            store_block_eqs(out1, j, q);
+            report_pivot(err, level + 1, bad.bad);
+        }
+    }
+}
+
+}  // namespace tpb

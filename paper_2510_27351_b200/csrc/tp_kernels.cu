@@ -42,6 +42,7 @@ __device__ unsigned long long g_trace[24];  // [0, 12) finishing solve, [12, 18)
 
 #include "tp_generic.cuh"
 #include "tp_final.cuh"
+#include "tp_fold.cuh"
 
 namespace tpb {
 
@@ -247,6 +248,38 @@ cudaError_t launch_fast(int64_t m, bool vec, int mode, const SysPtrs<T>& sys, in
 }
 
 
+// Level 0 + level 1 Stage 1 in one kernel (tp_fold.cuh). Requires full
+// level-0 blocks of a fixed shape, an even m1 whose blocks are exactly m1/2
+// level-0 blocks (no level-1 tail) and G = 8 (16 level-0 blocks per pass).
+// 5 CTAs/SM (96 registers): at 6 (80 registers) the pass loop spills and the
+// kernel runs 492 vs 485 us (C3, in-graph)
+static bool g_fold = true;
+
+bool fold_fits(int64_t m0, int64_t K0, int64_t n1, int64_t m1, int64_t K1) {
+    int L, G;
+    if (!g_fold || !fast_shape(m0, &L, &G) || G != 8) return false;
+    if (m1 < 4 || m1 % 2 != 0 || m1 > 64) return false;
+    return n1 == 2 * K0 && K1 * m1 == n1 && K1 >= kFoldL1Blocks;
+}
+
+template <class T>
+cudaError_t launch_fold(int64_t m0, bool vec, const SysPtrs<T>& sys, int64_t K0, const IfacePtrs<T>& out0,
+                        int64_t m1, int64_t K1, const IfacePtrs<T>& out1, unsigned long long* err, int level,
+                        cudaStream_t st) {
+    if (!fold_fits(m0, K0, 2 * K0, m1, K1)) return cudaErrorInvalidValue;
+    const int64_t grid = (K1 + kFoldL1Blocks - 1) / kFoldL1Blocks;
+    const size_t smem = (size_t)4 * kFoldL1Blocks * m1 * sizeof(T);
+#define TPB_FOLD(MM, LL)                                                                               \
+    if (m0 == MM) {                                                                                  \
+        auto k = vec ? k_fast_s1fold<T, LL, 8, true, 128, 5> : k_fast_s1fold<T, LL, 8, false, 128, 5>; \
+        return launch_k(level, k, (unsigned)grid, 128u, smem, st, sys, K0, out0, (int)m1, K1, out1, err, level); \
+    }
+    TPB_FOLD(40, 5)
+    TPB_FOLD(64, 8)
+#undef TPB_FOLD
+    return cudaErrorInvalidValue;
+}
+
 // Runtime-length register path (k_fast_rt): the G with ceil(m/G) <= 8, m/G >= 2.
 int fast_rt_G(int64_t m) {
     if (m < 2 || m > 256) return 0;
@@ -433,6 +466,7 @@ cudaError_t init_kernel_attributes() {
     if (const char* v = getenv("TPB_PDL")) g_pdl = atoi(v);
     if (const char* v = getenv("TPB_FINAL_CLUSTER")) g_final_cluster = atoi(v) != 0;
     if (const char* v = getenv("TPB_FUSE_LAST")) g_fuse_last = atoi(v) != 0;
+    if (const char* v = getenv("TPB_FOLD")) g_fold = atoi(v) != 0;
     cudaError_t e = set_smem_attributes<double>();
     if (e == cudaSuccess) e = set_smem_attributes<float>();
     g_lf_cs = probe_level_final_cluster();
@@ -480,6 +514,9 @@ cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsign
     template cudaError_t launch_final<T>(int, const SysPtrs<T>&, int64_t, const IfacePtrs<T>&,      \
                                          const T*, T*, unsigned long long*, int, cudaStream_t,      \
                                          const ShardLink*);                                         \
+    template cudaError_t launch_fold<T>(int64_t, bool, const SysPtrs<T>&, int64_t, const IfacePtrs<T>&, \
+                                        int64_t, int64_t, const IfacePtrs<T>&, unsigned long long*, int,   \
+                                        cudaStream_t);                                                  \
     template cudaError_t launch_level_final<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t,        \
                                                const IfacePtrs<T>&, T*,                             \
                                                unsigned long long*, int, cudaStream_t);             \

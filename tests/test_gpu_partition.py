@@ -529,3 +529,36 @@ def test_fused_deepest_level_random_shapes(tp, oracle_mod):
                 tp.RecursionPolicy(sizes))
             assert oracle_mod.rel_inf_diff(x32.astype(np.float64), ref) <= 1e-4, (case, n, sizes)
     assert fused >= 150  # most cases really take the fused kernel
+
+
+@pytest.mark.parametrize(
+    "n,sizes",
+    [
+        (1_000_000, [64, 10, 32]),    # C3's level-0/1 shape (m0 = 64, m1 = 10)
+        (800_000, [40, 8, 16]),       # m0 = 40 (5 x 8 lanes), m1 = 8
+        (1_280_000, [64, 4, 8, 16]),  # m1 = 4, deeper levels after the fold
+        (640_000, [64, 64, 8]),       # m1 = 64 (32 level-0 blocks per level-1 block)
+        (1_000_000, [64, 12, 16]),    # m1 = 12 with a level-1 tail: no fold (plain kernels)
+    ],
+)
+def test_folded_level_one(tp, oracle_mod, n, sizes):
+    """k_fast_s1fold (level 1's Stage 1 inside level 0's) against the oracle,
+    FP64 and FP32."""
+    s = oracle_mod.generate_system(n, 31)
+    ref = oracle_mod.solve_partition(s, sizes)
+    _check(oracle_mod, s, tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes)), ref)
+    x32 = tp.solve_partition(
+        tp.TridiagonalSystem(*(a.astype(np.float32) for a in (s.sub, s.diag, s.sup, s.rhs))), tp.RecursionPolicy(sizes))
+    assert oracle_mod.rel_inf_diff(x32.astype(np.float64), ref) <= 1e-4
+
+
+def test_folded_level_one_reports_zero_pivots(tp):
+    """A zero row in level 0 and one that only shows up in level 1's sweeps
+    (a level-0 block whose E2 pivot vanishes) raise ZeroPivotError."""
+    n = 1_000_000
+    sub, diag, sup, rhs = np.zeros(n), np.ones(n), np.zeros(n), np.ones(n)
+    for row in (12_345, 64 * 777 + 63):
+        d = diag.copy()
+        d[row] = 0.0
+        with pytest.raises(tp.ZeroPivotError):
+            tp.solve_partition(tp.TridiagonalSystem(sub, d, sup, rhs), tp.RecursionPolicy([64, 10, 32]))
