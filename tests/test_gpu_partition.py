@@ -537,13 +537,30 @@ def test_fused_deepest_level_random_shapes(tp, oracle_mod):
         (1_000_000, [64, 10, 32]),    # C3's level-0/1 shape (m0 = 64, m1 = 10)
         (800_000, [40, 8, 16]),       # m0 = 40 (5 x 8 lanes), m1 = 8
         (1_280_000, [64, 4, 8, 16]),  # m1 = 4, deeper levels after the fold
-        (640_000, [64, 64, 8]),       # m1 = 64 (32 level-0 blocks per level-1 block)
+        (655_360, [64, 64, 8]),       # m1 = 64 (32 level-0 blocks per level-1 block)
         (1_000_000, [64, 12, 16]),    # m1 = 12 with a level-1 tail: no fold (plain kernels)
     ],
 )
 def test_folded_level_one(tp, oracle_mod, n, sizes):
     """k_fast_s1fold (level 1's Stage 1 inside level 0's) against the oracle,
-    FP64 and FP32."""
+    FP64 and FP32; the launch list shows whether the fold ran."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2510_27351_b200._lib import TpError, lib
+
+    sd = tp.generate_system(n, 5, device=True)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    sz = np.asarray(sizes, dtype=np.int64)
+    kms, names, nk, err = (C.c_float * 64)(), C.create_string_buffer(64 * 32), C.c_int32(), TpError()
+    tp.context().set_stream(tp.torch_stream())
+    assert lib.tp_solve_profile_f64_dev(tp.context().handle, *sd._dev_ptrs(), n, sz.ctypes.data_as(C.POINTER(C.c_int64)),
+                                        len(sz), C.c_void_p(x.data_ptr()), kms, names, 64, C.byref(nk),
+                                        C.byref(err)) == 0
+    launched = [names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode() for i in range(nk.value)]
+    folded = n * 2 // sizes[0] % sizes[1] == 0
+    assert ("stage1_fold:L0" in launched) == folded, launched
     s = oracle_mod.generate_system(n, 31)
     ref = oracle_mod.solve_partition(s, sizes)
     _check(oracle_mod, s, tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes)), ref)

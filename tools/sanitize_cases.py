@@ -8,7 +8,8 @@
 Covers: k_fast (fixed shapes, both stages, vector and scalar loads), k_fast_rt
 (runtime chunk lengths), k_generic (tail blocks, m > 256), the fused deepest
 level + finishing solve (k_level_final_cl: cp.async staging, register and
-shared-memory sweeps, 16-CTA cluster), the cluster and the
+shared-memory sweeps, 16-CTA cluster), level 1 folded into level 0
+(k_fast_s1fold), the cluster and the
 single-CTA finishing solves (solve, sharded reduce / expand, the fused
 peer exchange on one rank), FP32, thomas_solve, the
 generator and the residual. Sizes are small so the sanitizer finishes in
@@ -40,6 +41,7 @@ def main():
         (100_003, [32, 10, 16]), # deeper recursion with tails (fused deepest level, m = 16)
         (20_001, [8]),           # fused deepest level, m = 8 register sweeps, (m + 1)-row tail
         (40_000, [64, 7]),       # fused deepest level, generic sweeps (odd m)
+        (160_000, [64, 10, 8]),  # level 1 folded into level 0 (k_fast_s1fold)
     ]
     worst = 0.0
     for n, sizes in cases:
