@@ -333,9 +333,12 @@ struct Runner {
             if (A.tail == 0 && A.kfull == A.K && B.tail == 0 && tpb::fold_fits(A.m, A.K, B.n, B.m, B.K)) {
                 const bool vec = aligned32(A.in.sub) && aligned32(A.in.diag) && aligned32(A.in.sup) &&
                                  aligned32(A.in.rhs);
-                check(tpb::launch_fold<T>(A.m, vec, A.in, A.K, A.iface, B.m, B.K, B.iface, ctx->d_err, 0, st));
-                after("stage1_fold", 0);
-                l = 2;
+                // level 2 too when its blocks are the fold CTAs' tiles (m2 = 32)
+                const bool f2 = top >= 3 && tpb::fold2_fits(B.K, p.levels[2].n, p.levels[2].m, p.levels[2].K);
+                check(tpb::launch_fold<T>(A.m, vec, A.in, A.K, A.iface, B.m, B.K, B.iface,
+                                          f2 ? &p.levels[2].iface : nullptr, ctx->d_err, 0, st));
+                after(f2 ? "stage1_fold2" : "stage1_fold", 0);
+                l = f2 ? 3 : 2;
             }
         }
         for (; l < top; ++l) stage(p.levels[l], (int)l, tpb::kStage1);

@@ -8,7 +8,8 @@
 // them to HBM (Stage 3 of level 1 reads that system), then 16 threads sweep
 // the 16 level-1 blocks from shared memory (leaf_smem, partition.hpp:90-124)
 // and write level 2's system. The separate Stage-1 kernel of level 1 and its
-// 100 MB re-read (C3) disappear.
+// 100 MB re-read (C3) disappear; with m2 = 32 (C3, C4) level 2's Stage-1
+// kernel and its tail branch as well (FOLD2).
 #pragma once
 #include "tp_fast.cuh"
 #include "tp_generic.cuh"
@@ -17,10 +18,14 @@ namespace tpb {
 
 constexpr int kFoldL1Blocks = 16;  // level-1 blocks per CTA
 
-template <class T, int L, int G, bool VEC, int THREADS, int MINB>
+// FOLD2: level 2 has m2 = 32 = 2 x 16, so its block j IS this CTA's 16
+// level-1 blocks' interface rows: the CTA also sweeps it (8 lanes x 4 rows in
+// warp 0, the k_fast lane tree) and writes level 3's system; level 2's
+// system is still written to HBM for its Stage 3.
+template <class T, int L, int G, bool VEC, int THREADS, int MINB, bool FOLD2 = false>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_fast_s1fold(SysPtrs<T> sys, int64_t nblocks0, IfacePtrs<T> out0, int m1, int64_t nblocks1,
-                  IfacePtrs<T> out1, unsigned long long* err, int level) {
+                  IfacePtrs<T> out1, IfacePtrs<T> out2, unsigned long long* err, int level) {
     static_assert(32 % G == 0, "G must divide the warp");
     constexpr int BP = THREADS / G;  // level-0 blocks per pass
     static_assert(BP == kFoldL1Blocks, "one pass = 16 level-0 blocks");
@@ -33,6 +38,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     T* sd = sc + rows1;
     const int c = (threadIdx.x & 31) % G;
     const int64_t blk0_base = (int64_t)blockIdx.x * kFoldL1Blocks * h;
+    __shared__ T s2[4][FOLD2 ? 2 * kFoldL1Blocks : 1];  // level-2 rows of this tile
     pdl_begin();
 
     for (int p = 0; p < h; ++p) {
@@ -74,6 +80,46 @@ __global__ void __launch_bounds__(THREADS, MINB)
             }
             store_block_eqs(out1, j, q);
             report_pivot(err, level + 1, bad.bad);
+            if constexpr (FOLD2) {
+                const int r = 2 * (int)threadIdx.x;
+                s2[0][r] = q.a1; s2[0][r + 1] = q.a2;
+                s2[1][r] = q.b1; s2[1][r + 1] = q.b2;
+                s2[2][r] = q.g1; s2[2][r + 1] = q.g2;
+                s2[3][r] = q.d1; s2[3][r + 1] = q.d2;
+            }
+        }
+    }
+    if constexpr (FOLD2) {
+        __syncwarp();  // the 16 writers are lanes 0-15 of warp 0
+        if (threadIdx.x < 32) {
+            const int64_t j2 = blockIdx.x;
+            const int64_t nb1 = nblocks1 - j2 * kFoldL1Blocks;  // level-1 blocks in this tile
+            const int lane = (int)threadIdx.x;
+            if (nb1 >= kFoldL1Blocks) {
+                // full level-2 block: 32 rows, lanes 0-7 hold 4 rows each
+                const bool act = lane < 8;
+                const int64_t row0 = j2 * 32 + 4 * lane;
+                LaneState<T, 4, 8, false> st;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    st.r.a[i] = act ? s2[0][4 * lane + i] : T(0);
+                    st.r.b[i] = act ? s2[1][4 * lane + i] : T(1);
+                    st.r.c[i] = act ? s2[2][4 * lane + i] : T(0);
+                    st.r.d[i] = act ? s2[3][4 * lane + i] : T(0);
+                }
+                lane_leaf<T, 4, 8, false>(st, row0);
+                lanes_tree<T, 4, 8, false>(st, lane & 7, row0);
+                if (act) {
+                    if (st.guard.tripped()) report_pivot(err, level + 2, row0);
+                    if (lane == 0) store_block_eqs(out2, j2, st.cur);
+                }
+            } else if (lane == 0) {
+                // the level-2 tail block (2 nb1 rows, nb1 >= 1)
+                RowGuard bad;
+                const Eq2<T> q = leaf_smem<T, false>(s2[0], s2[1], s2[2], s2[3], (int)(2 * nb1), j2 * 32, bad);
+                store_block_eqs(out2, j2, q);
+                report_pivot(err, level + 2, bad.bad);
+            }
         }
     }
 }

@@ -262,17 +262,27 @@ bool fold_fits(int64_t m0, int64_t K0, int64_t n1, int64_t m1, int64_t K1) {
     return n1 == 2 * K0 && K1 * m1 == n1 && K1 >= kFoldL1Blocks;
 }
 
+// level 2 folded as well: m2 == 32 makes level-2 block j exactly tile j
+static bool g_fold2 = true;
+bool fold2_fits(int64_t K1, int64_t n2, int64_t m2, int64_t K2) {
+    return g_fold2 && m2 == 2 * kFoldL1Blocks && n2 == 2 * K1 && K2 == (K1 + kFoldL1Blocks - 1) / kFoldL1Blocks;
+}
+
 template <class T>
 cudaError_t launch_fold(int64_t m0, bool vec, const SysPtrs<T>& sys, int64_t K0, const IfacePtrs<T>& out0,
-                        int64_t m1, int64_t K1, const IfacePtrs<T>& out1, unsigned long long* err, int level,
-                        cudaStream_t st) {
+                        int64_t m1, int64_t K1, const IfacePtrs<T>& out1, const IfacePtrs<T>* out2,
+                        unsigned long long* err, int level, cudaStream_t st) {
     if (!fold_fits(m0, K0, 2 * K0, m1, K1)) return cudaErrorInvalidValue;
     const int64_t grid = (K1 + kFoldL1Blocks - 1) / kFoldL1Blocks;
     const size_t smem = (size_t)4 * kFoldL1Blocks * m1 * sizeof(T);
+    const IfacePtrs<T> none{};
 #define TPB_FOLD(MM, LL)                                                                               \
     if (m0 == MM) {                                                                                  \
-        auto k = vec ? k_fast_s1fold<T, LL, 8, true, 128, 5> : k_fast_s1fold<T, LL, 8, false, 128, 5>; \
-        return launch_k(level, k, (unsigned)grid, 128u, smem, st, sys, K0, out0, (int)m1, K1, out1, err, level); \
+        auto k = out2 != nullptr                                                                     \
+                     ? (vec ? k_fast_s1fold<T, LL, 8, true, 128, 5, true> : k_fast_s1fold<T, LL, 8, false, 128, 5, true>) \
+                     : (vec ? k_fast_s1fold<T, LL, 8, true, 128, 5> : k_fast_s1fold<T, LL, 8, false, 128, 5>); \
+        return launch_k(level, k, (unsigned)grid, 128u, smem, st, sys, K0, out0, (int)m1, K1, out1,        \
+                        out2 != nullptr ? *out2 : none, err, level);                                 \
     }
     TPB_FOLD(40, 5)
     TPB_FOLD(64, 8)
@@ -467,6 +477,7 @@ cudaError_t init_kernel_attributes() {
     if (const char* v = getenv("TPB_FINAL_CLUSTER")) g_final_cluster = atoi(v) != 0;
     if (const char* v = getenv("TPB_FUSE_LAST")) g_fuse_last = atoi(v) != 0;
     if (const char* v = getenv("TPB_FOLD")) g_fold = atoi(v) != 0;
+    if (const char* v = getenv("TPB_FOLD2")) g_fold2 = atoi(v) != 0;
     cudaError_t e = set_smem_attributes<double>();
     if (e == cudaSuccess) e = set_smem_attributes<float>();
     g_lf_cs = probe_level_final_cluster();
@@ -515,8 +526,8 @@ cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsign
                                          const T*, T*, unsigned long long*, int, cudaStream_t,      \
                                          const ShardLink*);                                         \
     template cudaError_t launch_fold<T>(int64_t, bool, const SysPtrs<T>&, int64_t, const IfacePtrs<T>&, \
-                                        int64_t, int64_t, const IfacePtrs<T>&, unsigned long long*, int,   \
-                                        cudaStream_t);                                                  \
+                                        int64_t, int64_t, const IfacePtrs<T>&, const IfacePtrs<T>*,        \
+                                        unsigned long long*, int, cudaStream_t);                        \
     template cudaError_t launch_level_final<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t,        \
                                                const IfacePtrs<T>&, T*,                             \
                                                unsigned long long*, int, cudaStream_t);             \

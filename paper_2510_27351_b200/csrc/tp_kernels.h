@@ -81,11 +81,13 @@ cudaError_t launch_final(int mode, const SysPtrs<T>& sys, int64_t n, const Iface
                          const T* xi, T* x, unsigned long long* err, int level, cudaStream_t st,
                          const ShardLink* link = nullptr);
 // Level 0's Stage 1 with level 1's folded in (k_fast_s1fold, tp_fold.cuh).
+// With out2 (fold2_fits: m2 == 32) level 2's Stage 1 is folded in as well.
 bool fold_fits(int64_t m0, int64_t K0, int64_t n1, int64_t m1, int64_t K1);
+bool fold2_fits(int64_t K1, int64_t n2, int64_t m2, int64_t K2);
 template <class T>
 cudaError_t launch_fold(int64_t m0, bool vec, const SysPtrs<T>& sys, int64_t K0, const IfacePtrs<T>& out0,
-                        int64_t m1, int64_t K1, const IfacePtrs<T>& out1, unsigned long long* err, int level,
-                        cudaStream_t st);
+                        int64_t m1, int64_t K1, const IfacePtrs<T>& out1, const IfacePtrs<T>* out2,
+                        unsigned long long* err, int level, cudaStream_t st);
 // The deepest level fused with the finishing solve (k_level_final_cl):
 // level_final_fits says whether a level of n rows in K blocks of m fits the
 // cluster's shared memory; launch_level_final returns cudaErrorInvalidValue

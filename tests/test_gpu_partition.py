@@ -539,6 +539,9 @@ def test_fused_deepest_level_random_shapes(tp, oracle_mod):
         (1_280_000, [64, 4, 8, 16]),  # m1 = 4, deeper levels after the fold
         (655_360, [64, 64, 8]),       # m1 = 64 (32 level-0 blocks per level-1 block)
         (1_000_000, [64, 12, 16]),    # m1 = 12 with a level-1 tail: no fold (plain kernels)
+        (4_000_000, [64, 10, 32, 16]),  # level 2 folded too (m2 = 32): tail tile of 10 level-1 blocks
+        (2_048_000, [64, 8, 32, 8]),    # level 2 folded, no level-2 tail
+        (1_600_064, [32, 10, 32, 16]),  # m0 = 32 (8 x 4 lanes): no fold
     ],
 )
 def test_folded_level_one(tp, oracle_mod, n, sizes):
@@ -559,8 +562,9 @@ def test_folded_level_one(tp, oracle_mod, n, sizes):
                                         len(sz), C.c_void_p(x.data_ptr()), kms, names, 64, C.byref(nk),
                                         C.byref(err)) == 0
     launched = [names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode() for i in range(nk.value)]
-    folded = n * 2 // sizes[0] % sizes[1] == 0
-    assert ("stage1_fold:L0" in launched) == folded, launched
+    folded = sizes[0] in (40, 64) and n % sizes[0] == 0 and n * 2 // sizes[0] % sizes[1] == 0
+    assert ("stage1_fold:L0" in launched or "stage1_fold2:L0" in launched) == folded, launched
+    assert ("stage1_fold2:L0" in launched) == (folded and len(sizes) >= 3 and sizes[2] == 32), launched
     s = oracle_mod.generate_system(n, 31)
     ref = oracle_mod.solve_partition(s, sizes)
     _check(oracle_mod, s, tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes)), ref)
