@@ -42,7 +42,7 @@ def main():
         (20_001, [8]),           # fused deepest level, m = 8 register sweeps, (m + 1)-row tail
         (40_000, [64, 7]),       # fused deepest level, generic sweeps (odd m)
         (160_000, [64, 10, 8]),  # level 1 folded into level 0 (k_fast_s1fold)
-        (640_000, [64, 10, 32]), # levels 1 and 2 folded (FOLD2, level-2 tail tile)
+        (640_000, [64, 10, 32]), # levels 1 and 2 folded (FOLD2)
     ]
     worst = 0.0
     for n, sizes in cases:
