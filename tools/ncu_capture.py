@@ -106,7 +106,8 @@ def summarize(rep: str, out: str, md: str = None):
                          f"{v['dram_write_bytes'] / 1e6:.1f} | {v['dram_pct_of_peak']:.1f} | {v['warps_active_pct']:.1f} | "
                          f"{v['fp64_pipe_pct']:.1f} | {v['regs']:.0f} | {v['grid']:.0f}x{v['block']:.0f} |")
         lines.append(f"\nSum of launches: {tot:.4f} ms")
-        s1, s3 = res.get("stage1:L0") or res.get("stage1_fold:L0"), res.get("stage3:L0")
+        s1_key = next((k for k in res if k.startswith("stage1") and k.endswith(":L0")), None)
+        s1, s3 = res.get(s1_key) if s1_key else None, res.get("stage3:L0")
         if s1 and s3:
             lines.append(f"Level-0 Stage 1 + Stage 3 = {100 * (s1['duration_ms'] + s3['duration_ms']) / tot:.1f}% "
                          f"of the launch sum; Stage 3 L0 alone {100 * s3['duration_ms'] / tot:.1f}%.")
@@ -114,7 +115,8 @@ def summarize(rep: str, out: str, md: str = None):
             lines.append(f"Stage 3 L0: algorithmic {40 * n / 1e9:.3f} GB (40 B/unknown) vs DRAM traffic "
                          f"{s3['dram_bytes'] / 1e9:.3f} GB; {s3['dram_bytes'] / s3['duration_ms'] / 1e6:.0f} GB/s "
                          f"under ncu.")
-            lines.append(f"Stage 1 L0{' (level 1 folded in)' if 'stage1_fold:L0' in res else ''}: algorithmic "
+            folded = {"stage1_fold:L0": " (level 1 folded in)", "stage1_fold2:L0": " (levels 1 and 2 folded in)"}
+            lines.append(f"Stage 1 L0{folded.get(s1_key, '')}: algorithmic "
                          f"{32 * n / 1e9:.3f} GB read + {s1['dram_write_bytes'] / 1e9:.3f} "
                          f"GB interfaces written vs DRAM {s1['dram_bytes'] / 1e9:.3f} GB; "
                          f"{s1['dram_bytes'] / s1['duration_ms'] / 1e6:.0f} GB/s under ncu.")
