@@ -18,6 +18,33 @@ namespace tpb {
 
 constexpr int kFoldL1Blocks = 16;  // level-1 blocks per CTA
 
+// Stores of the small deeper-level systems (C3: 20 MB + 1.25 MB) marked
+// L2 evict_last so they survive the level-0 stream until their readers.
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void store_pair_keep(double* p, double x0, double x1, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(x0), "d"(x1), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void store_pair_keep(float* p, float x0, float x1, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(x0), "f"(x1), "l"(pol) : "memory");
+}
+template <class T>
+__device__ __forceinline__ void store_block_eqs_keep(const IfacePtrs<T>& out, int64_t blk, const Eq2<T>& q, bool keep) {
+    if (!keep) {
+        store_block_eqs(out, blk, q);
+        return;
+    }
+    const uint64_t pol = l2_keep_policy();
+    const int64_t o = 2 * blk;
+    store_pair_keep(out.sub + o, q.a1, q.a2, pol);
+    store_pair_keep(out.diag + o, q.b1, q.b2, pol);
+    store_pair_keep(out.sup + o, q.g1, q.g2, pol);
+    store_pair_keep(out.rhs + o, q.d1, q.d2, pol);
+}
+
 // FOLD2: level 2 has m2 = 32 = 2 x 16, so its block j IS this CTA's 16
 // level-1 blocks' interface rows: the CTA also sweeps it (8 lanes x 4 rows in
 // warp 0, the k_fast lane tree) and writes level 3's system; level 2's
@@ -25,7 +52,7 @@ constexpr int kFoldL1Blocks = 16;  // level-1 blocks per CTA
 template <class T, int L, int G, bool VEC, int THREADS, int MINB, bool FOLD2 = false>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_fast_s1fold(SysPtrs<T> sys, int64_t nblocks0, IfacePtrs<T> out0, int m1, int64_t nblocks1,
-                  IfacePtrs<T> out1, IfacePtrs<T> out2, unsigned long long* err, int level) {
+                  IfacePtrs<T> out1, IfacePtrs<T> out2, unsigned long long* err, int level, int keep) {
     static_assert(32 % G == 0, "G must divide the warp");
     constexpr int BP = THREADS / G;  // level-0 blocks per pass
     static_assert(BP == kFoldL1Blocks, "one pass = 16 level-0 blocks");
@@ -78,7 +105,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             } else {
                 q = leaf_smem<T, false>(sa + o, sb + o, sc + o, sd + o, m1, j * m1, bad);
             }
-            store_block_eqs(out1, j, q);
+            store_block_eqs_keep(out1, j, q, keep != 0);
             report_pivot(err, level + 1, bad.bad);
             if constexpr (FOLD2) {
                 const int r = 2 * (int)threadIdx.x;
@@ -111,13 +138,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 lanes_tree<T, 4, 8, false>(st, lane & 7, row0);
                 if (act) {
                     if (st.guard.tripped()) report_pivot(err, level + 2, row0);
-                    if (lane == 0) store_block_eqs(out2, j2, st.cur);
+                    if (lane == 0) store_block_eqs_keep(out2, j2, st.cur, keep != 0);
                 }
             } else if (lane == 0) {
                 // the level-2 tail block (2 nb1 rows, nb1 >= 1)
                 RowGuard bad;
                 const Eq2<T> q = leaf_smem<T, false>(s2[0], s2[1], s2[2], s2[3], (int)(2 * nb1), j2 * 32, bad);
-                store_block_eqs(out2, j2, q);
+                store_block_eqs_keep(out2, j2, q, keep != 0);
                 report_pivot(err, level + 2, bad.bad);
             }
         }

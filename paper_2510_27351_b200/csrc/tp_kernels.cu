@@ -264,6 +264,7 @@ bool fold_fits(int64_t m0, int64_t K0, int64_t n1, int64_t m1, int64_t K1) {
 
 // level 2 folded as well: m2 == 32 makes level-2 block j exactly tile j
 static bool g_fold2 = true;
+static int g_fold_keep = 1;  // L2 evict_last on the deeper systems the fold writes (TPB_FOLD_KEEP)
 bool fold2_fits(int64_t K1, int64_t n2, int64_t m2, int64_t K2) {
     return g_fold2 && m2 == 2 * kFoldL1Blocks && n2 == 2 * K1 && K2 == (K1 + kFoldL1Blocks - 1) / kFoldL1Blocks;
 }
@@ -282,7 +283,7 @@ cudaError_t launch_fold(int64_t m0, bool vec, const SysPtrs<T>& sys, int64_t K0,
                      ? (vec ? k_fast_s1fold<T, LL, 8, true, 128, 5, true> : k_fast_s1fold<T, LL, 8, false, 128, 5, true>) \
                      : (vec ? k_fast_s1fold<T, LL, 8, true, 128, 5> : k_fast_s1fold<T, LL, 8, false, 128, 5>); \
         return launch_k(level, k, (unsigned)grid, 128u, smem, st, sys, K0, out0, (int)m1, K1, out1,        \
-                        out2 != nullptr ? *out2 : none, err, level);                                 \
+                        out2 != nullptr ? *out2 : none, err, level, g_fold_keep);                    \
     }
     TPB_FOLD(40, 5)
     TPB_FOLD(64, 8)
@@ -478,6 +479,7 @@ cudaError_t init_kernel_attributes() {
     if (const char* v = getenv("TPB_FUSE_LAST")) g_fuse_last = atoi(v) != 0;
     if (const char* v = getenv("TPB_FOLD")) g_fold = atoi(v) != 0;
     if (const char* v = getenv("TPB_FOLD2")) g_fold2 = atoi(v) != 0;
+    if (const char* v = getenv("TPB_FOLD_KEEP")) g_fold_keep = atoi(v);
     cudaError_t e = set_smem_attributes<double>();
     if (e == cudaSuccess) e = set_smem_attributes<float>();
     g_lf_cs = probe_level_final_cluster();
