@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TP_ABI_VERSION 1
+#define TP_ABI_VERSION 2
 
 /* Error classes of include/tridpart/errors.hpp:7-96. */
 typedef enum tp_status {
@@ -52,7 +52,8 @@ typedef enum tp_status {
 typedef struct tp_error {
     int32_t code;   /* tp_status */
     int32_t level;  /* partition level of a zero pivot (0 = the input system) */
-    int64_t row;    /* ZeroPivotError::row() (row index within that level) */
+    int64_t row;    /* ZeroPivotError::row() (row index within that level's system, in the
+                       reference's sweep order); BadNumberError: the line */
     char msg[256];
 } tp_error;
 
@@ -83,6 +84,12 @@ tp_status tp_solve_partition_f64_dev(tp_ctx* ctx, const double* sub, const doubl
                                      const double* super, const double* rhs, int64_t n,
                                      const int64_t* sizes, int32_t nsizes, double* x, void* stream,
                                      tp_error* err);
+/* Zero pivots (host and device calls): err->row / err->level are the ones
+ * ZeroPivotError carries in the reference — the first failing pivot of its
+ * sequential order (levels 0..depth, blocks in order, up-sweep then
+ * down-sweep; then thomas_solve of the deepest interface), found by replaying
+ * the reference's arithmetic on the device over the level systems of the
+ * failed solve. tp_check_device_error needs the last solve's buffers alive. */
 tp_status tp_check_device_error(tp_ctx* ctx, tp_error* err);
 
 /* Host pointers, asynchronous on `stream` (NULL = ctx stream): the H2D copies,
@@ -97,7 +104,9 @@ tp_status tp_solve_partition_f64_async(tp_ctx* ctx, const double* sub, const dou
 
 /* Observer overload solve_partition(sys, policy, on_interface) — partition.hpp:235-242,
  * hook at :206. Host pointers; after the solve, `cb` receives each level's
- * assembled interface system (host copies, valid during the call), level 0 first. */
+ * assembled interface system (host copies, valid during the call), level 0 first.
+ * On a zero pivot at level l (err->level) the levels the reference completed
+ * before it (0 .. l-1) are delivered, then the error is returned. */
 typedef void (*tp_interface_cb)(int64_t level, int64_t n, const double* sub, const double* diag,
                                 const double* super, const double* rhs, void* user);
 tp_status tp_solve_partition_observe_f64(tp_ctx* ctx, const double* sub, const double* diag,
@@ -128,7 +137,10 @@ tp_status tp_thomas_solve_f32(tp_ctx* ctx, const float* sub, const float* diag, 
                               const float* rhs, int64_t n, float* x, tp_error* err);
 tp_status tp_residual_inf_f32_dev(tp_ctx* ctx, const float* sub, const float* diag,
                                   const float* super, const float* rhs, int64_t n, const float* x,
-                                  double* out, tp_error* err);
+                                  double* out, void* stream, tp_error* err);
+tp_status tp_reduce_block_f32(tp_ctx* ctx, const float* sub, const float* diag, const float* super,
+                              const float* rhs, int64_t n, int64_t start, int64_t end, float* eq8, float* a,
+                              float* beta, float* gamma, float* delta, tp_error* err);
 
 /* thomas_solve(sys) — tridiagonal.hpp:52-72. Same solution, computed by the
  * device finishing solver (exact parallel elimination, not a sequential sweep). */
@@ -136,10 +148,22 @@ tp_status tp_thomas_solve_f64(tp_ctx* ctx, const double* sub, const double* diag
                               const double* super, const double* rhs, int64_t n, double* x,
                               tp_error* err);
 
-/* residual_inf(sys, x) — tridiagonal.hpp:74-87, on device pointers (synchronous). */
+/* residual_inf(sys, x) — tridiagonal.hpp:74-87, on device pointers; runs on
+ * `stream` (NULL = ctx stream, so ordered after work the caller queued there)
+ * and returns when the value is on the host. */
 tp_status tp_residual_inf_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
                                   const double* super, const double* rhs, int64_t n,
-                                  const double* x, double* out, tp_error* err);
+                                  const double* x, double* out, void* stream, tp_error* err);
+
+/* reduce_block(sys, Block{start, end}) — partition.hpp:77-126. Host pointers to
+ * the whole system (n rows); computed on the device with the reference's own
+ * sequential arithmetic. eq8 = alpha1 beta1 gamma1 delta1 alpha2 beta2 gamma2
+ * delta2; a / beta / gamma / delta (each end-start values, may be NULL) = the
+ * ReducedBlock up-sweep vectors by offset from start (entry end-start-1 = 0).
+ * ZeroPivotError row = the system row; block length < 2 -> INVALID_SIZE. */
+tp_status tp_reduce_block_f64(tp_ctx* ctx, const double* sub, const double* diag, const double* super,
+                              const double* rhs, int64_t n, int64_t start, int64_t end, double* eq8,
+                              double* a, double* beta, double* gamma, double* delta, tp_error* err);
 
 /* ------------------------------------------------ sharded (multi-GPU) solve
  * Contiguous shard [row0, row0+n_local) of a global system, one rank per GPU.
@@ -190,6 +214,13 @@ tp_status tp_shard_prepare_f64_dev(tp_ctx* ctx, const double* sub, const double*
                                    tp_error* err);
 
 /* --------------------------------------------------- synthetic inputs */
+/* generate_system(n, seed, delta) — bench.hpp:68-93, BIT-IDENTICAL to the
+ * reference: std::mt19937_64(seed), libstdc++ uniform_real_distribution<double>
+ * (-1, 1) and bernoulli_distribution(0.5), drawn sub, super, rhs, flip per row.
+ * Host code, host arrays of n doubles. n < 2 or delta <= 1 -> INVALID_SIZE. */
+tp_status tp_generate_system_f64(int64_t n, uint64_t seed, double delta, double* sub, double* diag,
+                                 double* super, double* rhs, tp_error* err);
+
 /* Device analogue of generate_system(n, seed, delta) — bench.hpp:68-93: same
  * distributions, counter-based (rows [row0, row0+n) of an n_global system),
  * not bit-identical to std::mt19937_64. */

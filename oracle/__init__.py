@@ -162,9 +162,13 @@ def generate_system(n: int, seed: int, delta: float = 1.5, impl: str = "port") -
 
 
 class OracleZeroPivot(Exception):
-    def __init__(self, row: int):
-        super().__init__(f"zero pivot at row {row}")
+    """ZeroPivotError(row) of the oracle; ``level`` = the system the row indexes
+    (0 = input, l = interface of level l-1), when known."""
+
+    def __init__(self, row: int, level: Optional[int] = None):
+        super().__init__(f"zero pivot at row {row}" + ("" if level is None else f" (level {level})"))
         self.row = row
+        self.level = level
 
 
 def _status(st: int):
@@ -177,23 +181,37 @@ def _status(st: int):
 
 def solve_partition(sys: System, sizes: Sequence[int], impl: str = "port",
                     observer: Optional[Callable] = None) -> np.ndarray:
-    """solve_partition (partition.hpp:235-248); observer(level, sub, diag, sup, rhs)."""
+    """solve_partition (partition.hpp:235-248); observer(level, sub, diag, sup, rhs).
+
+    A zero pivot raises OracleZeroPivot(row, level): the port reports the level
+    itself; for the reference (impl="ref") the level is the number of observer
+    calls made before the throw — the reference calls the observer once per
+    assembled level (partition.hpp:205-206), so a throw in level l's Stage 1
+    comes after l calls and one in the final thomas_solve after depth+1.
+    NOTE: the reference std::terminate()s on a zero pivot inside a parallel
+    region (K >= 128 blocks at that level): callers keep K < 128 for impl="ref"."""
     x = np.empty(sys.n, dtype=np.float64)
     sz = np.asarray(sizes, dtype=np.int64)
-    cb = OBSERVER(0)
-    if observer is not None:
-        def _cb(level, n, a, b, c, d, _u):
+    calls = [0]
+
+    def _cb(level, n, a, b, c, d, _u):
+        calls[0] += 1
+        if observer is not None:
             observer(int(level), np.ctypeslib.as_array(a, (n,)).copy(),
                      np.ctypeslib.as_array(b, (n,)).copy(), np.ctypeslib.as_array(c, (n,)).copy(),
                      np.ctypeslib.as_array(d, (n,)).copy())
-        cb = OBSERVER(_cb)
+    cb = OBSERVER(_cb) if (observer is not None or impl != "port") else OBSERVER(0)
     if impl == "port":
         lvl = C.c_int64(0)
         st = port().orc_solve_partition(sys.n, *sys.ptrs(), sz.ctypes.data_as(_I64), len(sz),
                                         _dp(x), cb, None, C.byref(lvl))
+        if st >= 0:
+            raise OracleZeroPivot(int(st), int(lvl.value))
     else:
         st = ref().ref_solve_partition(sys.n, *sys.ptrs(), sz.ctypes.data_as(_I64), len(sz),
                                        _dp(x), cb, None)
+        if st >= 0:
+            raise OracleZeroPivot(int(st), calls[0])
     _status(st)
     return x
 

@@ -9,6 +9,7 @@ from .tridpart import (  # noqa: F401
     generate_system,
     kMaxRecursionDepth, kModelFormatVersion, kPivotFloor, load_model, make_plan, plan_levels,
     predict, predicted_policy, read_observations, recursion_sizes, residual_inf, save_model,
-    solve_partition, solve_partition_async, thomas_solve, torch_stream)
+    solve_partition, solve_partition_async, thomas_solve, torch_stream,
+    ReducedBlock, reduce_block, assemble_interface, back_substitute)
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

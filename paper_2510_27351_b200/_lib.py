@@ -45,6 +45,7 @@ EXPORTS = [
     "tp_residual_inf_f32_dev", "tp_generate_system_f32_dev", "tp_solve_partition_f64_async",
     "tp_solve_partition_f32_async", "tp_shard_mailbox", "tp_ipc_get_handle", "tp_ipc_open_handle",
     "tp_shard_attach", "tp_shard_solve_f64_dev", "tp_shard_prepare_f64_dev",
+    "tp_reduce_block_f64", "tp_reduce_block_f32", "tp_generate_system_f64",
 ]
 
 
@@ -54,6 +55,8 @@ def _load():
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(make -C paper_2510_27351_b200/csrc). There is no CPU fallback.")
     lib = C.CDLL(LIB_PATH)
+    if lib.tp_abi_version() != 2:
+        raise ImportError(f"{LIB_PATH}: C-ABI version {lib.tp_abi_version()}, this package needs 2 (rebuild)")
     vp, E = C.c_void_p, C.POINTER(TpError)
     sig = {
         "tp_abi_version": (C.c_int32, []),
@@ -69,7 +72,7 @@ def _load():
         "tp_solve_partition_observe_f64": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32,
                                                      vp, INTERFACE_CB, vp, E]),
         "tp_thomas_solve_f64": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, E]),
-        "tp_residual_inf_f64_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, _D, E]),
+        "tp_residual_inf_f64_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, _D, vp, E]),
         "tp_shard_reduce_f64_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
                                               vp, E]),
         "tp_shard_finish_f64_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
@@ -99,7 +102,12 @@ def _load():
                                                    vp, E]),
         "tp_solve_partition_f32_async": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
                                                    vp, E]),
-        "tp_residual_inf_f32_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, _D, E]),
+        "tp_residual_inf_f32_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, _D, vp, E]),
+        "tp_reduce_block_f64": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, C.c_int64, C.c_int64, vp, vp, vp,
+                                          vp, vp, E]),
+        "tp_reduce_block_f32": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, C.c_int64, C.c_int64, vp, vp, vp,
+                                          vp, vp, E]),
+        "tp_generate_system_f64": (C.c_int, [C.c_int64, C.c_uint64, C.c_double, vp, vp, vp, vp, E]),
         "tp_shard_mailbox": (C.c_int, [vp, C.c_int32, C.POINTER(vp), E]),
         "tp_ipc_get_handle": (C.c_int, [vp, vp, C.POINTER(C.c_uint8), E]),
         "tp_ipc_open_handle": (C.c_int, [vp, C.POINTER(C.c_uint8), C.POINTER(vp), E]),

@@ -81,10 +81,17 @@ struct Level {
     int64_t kfull = 0;  // blocks of exactly m rows
     int64_t tail = 0;   // length of the final block when != m (0 = none)
     bool internal = false;
+    // long-block chain (tp_split.cuh): a split level cuts every block into
+    // nsub (tail: nsub_tail) chunks and writes their E1/E2 pairs as a finer
+    // system of out_rows rows; the level after it keeps the block boundaries
+    bool split = false;
+    int64_t nsub = 0, nsub_tail = 0;
+    int64_t out_rows = 0;   // rows of the system this level writes (2K, or the finer system)
+    int policy_level = -1;  // RecursionPolicy level this plan level belongs to (-1: device-internal)
     // bound pointers
     SysPtrs<T> in{};
     T* x_out = nullptr;    // solution of this level's system
-    IfacePtrs<T> iface{};  // next level's system (2K rows)
+    IfacePtrs<T> iface{};  // next level's system (out_rows rows)
     T* x_iface = nullptr;
 };
 
@@ -98,6 +105,35 @@ struct Plan {
 };
 
 inline size_t pad32(size_t v) { return (v + 31) & ~size_t(31); }
+
+// A level whose blocks are too long for shared-memory staging becomes a chain
+// of split levels ending in a level with the original block boundaries
+// (tp_split.cuh): each split cuts every block into chunks of <= kSplitRows
+// rows and hands the next level 2 rows per chunk.
+inline bool needs_split(int64_t kfull, int64_t m, int64_t tail) {
+    return (kfull > 0 && m > tpb::kSplitAbove) || tail > tpb::kSplitAbove + 1;
+}
+
+template <class T>
+void push_chain(Plan<T>& p, Level<T> L, size_t& ws) {
+    while (needs_split(L.kfull, L.m, L.tail)) {
+        Level<T> S = L;
+        S.split = true;
+        S.nsub = L.kfull > 0 ? (L.m + tpb::kSplitRows - 1) / tpb::kSplitRows : 0;
+        S.nsub_tail = L.tail > 0 ? (L.tail + tpb::kSplitRows - 1) / tpb::kSplitRows : 0;
+        S.out_rows = 2 * (L.kfull * S.nsub + S.nsub_tail);
+        ws += 5 * pad32((size_t)S.out_rows);
+        p.levels.push_back(S);
+        Level<T> M = L;
+        M.n = S.out_rows;
+        M.m = L.kfull > 0 ? 2 * S.nsub : 2 * S.nsub_tail;
+        M.tail = 2 * S.nsub_tail;
+        L = M;
+    }
+    L.out_rows = 2 * L.K;
+    ws += 5 * pad32((size_t)L.out_rows);
+    p.levels.push_back(L);
+}
 
 // fused = the plan is for solve_body, which runs the deepest level and the
 // finishing solve as one kernel when that level fits k_level_final_cl: then
@@ -116,6 +152,7 @@ void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p, boo
         L.n = cur;
         L.m = sizes[lvl];
         L.K = plan_blocks(cur, L.m);
+        L.policy_level = lvl;
         const int64_t last_len = cur - (L.K - 1) * L.m;
         if (L.m >= cur) {
             L.kfull = (cur == L.m) ? 1 : 0;
@@ -127,14 +164,13 @@ void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p, boo
             L.kfull = L.K - 1;
             L.tail = last_len;
         }
-        ws += 5 * pad32((size_t)(2 * L.K));
-        p.levels.push_back(L);
+        push_chain(p, L, ws);
         cur = 2 * L.K;
         if (lvl == nsizes - 1) break;
         ++lvl;
     }
     // device-internal levels so the finishing solve fits one cluster
-    const bool last_fused = fused && !p.levels.empty() &&
+    const bool last_fused = fused && !p.levels.empty() && !p.levels.back().split &&
                             tpb::level_final_fits(p.levels.back().n, p.levels.back().m, p.levels.back().K, sizeof(T));
     while (!last_fused && cur > tpb::kFinalCap) {
         Level<T> L;
@@ -147,6 +183,7 @@ void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p, boo
         L.kfull = (last_len == L.m) ? L.K : L.K - 1;
         L.tail = (last_len == L.m) ? 0 : last_len;
         L.internal = true;
+        L.out_rows = 2 * L.K;
         ws += 5 * pad32((size_t)(2 * L.K));
         p.levels.push_back(L);
         cur = 2 * L.K;
@@ -164,7 +201,7 @@ void bind_plan(Plan<T>& p, const SysPtrs<T>& sys, T* x, void* ws) {
     for (auto& L : p.levels) {
         L.in = in;
         L.x_out = xo;
-        const size_t k2 = pad32((size_t)(2 * L.K));
+        const size_t k2 = pad32((size_t)L.out_rows);
         L.iface.sub = w;
         L.iface.diag = w + k2;
         L.iface.sup = w + 2 * k2;
@@ -217,6 +254,16 @@ struct tp_ctx {
     void* dsys = nullptr;                 // host-path staging (5 arrays)
     size_t dsys_cap = 0;                  // bytes
     int64_t last_launches = 0;
+    // The last solve whose zero pivot tp_check_device_error / the synchronous
+    // calls may have to locate in the reference's order (diagnose_pivot).
+    struct LastSolve {
+        int kind = 0;  // 0 none / not diagnosable, 1 solve_partition, 2 thomas_solve
+        bool f32 = false;
+        int64_t n = 0;
+        std::vector<int64_t> sizes;
+        const void* in[4] = {nullptr, nullptr, nullptr, nullptr};
+        void* x = nullptr;
+    } last;
     struct GraphEntry {
         std::vector<int64_t> key;
         cudaGraphExec_t exec = nullptr;
@@ -256,7 +303,11 @@ struct Runner {
     void main_part(const Level<T>& L, int level, int mode) {
         const bool s1 = (mode == tpb::kStage1);
         int fl, fg;
-        if (tpb::fast_shape(L.m, &fl, &fg)) {
+        if (L.split) {
+            check(tpb::launch_split<T>(mode, L.in, 0, L.kfull, L.m, L.nsub, 0, L.iface, L.x_iface, L.x_out,
+                                       ctx->d_err, level, st));
+            after(s1 ? "stage1s" : "stage3s", level);
+        } else if (tpb::fast_shape(L.m, &fl, &fg)) {
             const bool vec = aligned32(L.in.sub) && aligned32(L.in.diag) && aligned32(L.in.sup) &&
                              aligned32(L.in.rhs) && (s1 || aligned32(L.x_out));
             check(tpb::launch_fast<T>(L.m, vec, mode, L.in, L.kfull, L.iface, L.x_iface, L.x_out,
@@ -278,6 +329,12 @@ struct Runner {
         }
     }
     void tail_part(const Level<T>& L, int level, int mode, cudaStream_t s) {
+        if (L.split) {
+            check(tpb::launch_split<T>(mode, L.in, L.kfull * L.m, 1, L.tail, L.nsub_tail, L.kfull * L.nsub, L.iface,
+                                       L.x_iface, L.x_out, ctx->d_err, level, s));
+            after(mode == tpb::kStage1 ? "stage1st" : "stage3st", level);
+            return;
+        }
         // short Stage-3 tails on one lane (no tree, no cross-lane barriers):
         // 4.8 -> 3.9 us for the 8-row tail on the critical path of C3 level 3;
         // Stage-1 tails run beside their main kernel and keep the 2-lane form
@@ -323,18 +380,19 @@ struct Runner {
     // interface is still written out (for the observer), never read back.
     void solve_body(const Plan<T>& p) {
         const size_t nl = p.levels.size();
-        const bool fuse = nl > 0 && tpb::level_final_fits(p.levels.back().n, p.levels.back().m,
-                                                          p.levels.back().K, sizeof(T));
+        const bool fuse = nl > 0 && !p.levels.back().split &&
+                          tpb::level_final_fits(p.levels.back().n, p.levels.back().m, p.levels.back().K, sizeof(T));
         const size_t top = fuse ? nl - 1 : nl;
         size_t l = 0;
         if (top >= 2) {  // level 1's Stage 1 folded into level 0's (k_fast_s1fold)
             const Level<T>& A = p.levels[0];
             const Level<T>& B = p.levels[1];
-            if (A.tail == 0 && A.kfull == A.K && B.tail == 0 && tpb::fold_fits(A.m, A.K, B.n, B.m, B.K)) {
+            if (!A.split && !B.split && A.tail == 0 && A.kfull == A.K && B.tail == 0 &&
+                tpb::fold_fits(A.m, A.K, B.n, B.m, B.K)) {
                 const bool vec = aligned32(A.in.sub) && aligned32(A.in.diag) && aligned32(A.in.sup) &&
                                  aligned32(A.in.rhs);
                 // level 2 too when its blocks are the fold CTAs' tiles (m2 = 32)
-                const bool f2 = top >= 3 && tpb::fold2_fits(B.K, p.levels[2].n, p.levels[2].m, p.levels[2].K);
+                const bool f2 = top >= 3 && !p.levels[2].split && tpb::fold2_fits(B.K, p.levels[2].n, p.levels[2].m, p.levels[2].K);
                 check(tpb::launch_fold<T>(A.m, vec, A.in, A.K, A.iface, B.m, B.K, B.iface,
                                           f2 ? &p.levels[2].iface : nullptr, ctx->d_err, 0, st));
                 after(f2 ? "stage1_fold2" : "stage1_fold", 0);
@@ -448,6 +506,9 @@ tp_status ensure_dsys(tp_ctx* ctx, int64_t n, T** arrays, tp_error* err) {
     return TP_OK;
 }
 
+template <class T>
+tp_status diagnose_pivot(tp_ctx* ctx, int64_t dev_row, int32_t dev_level, tp_error* err);
+
 tp_status decode_device_error(tp_ctx* ctx, tp_error* err) {
     const unsigned long long code = *ctx->h_err;
     if (code == tpb::kNoError) return TP_OK;
@@ -457,6 +518,12 @@ tp_status decode_device_error(tp_ctx* ctx, tp_error* err) {
         set_err(err, TP_ERR_NCCL, "peer exchange timed out waiting for rank " + std::to_string(row), row, -1);
         return TP_ERR_NCCL;
     }
+    // a pivot below the floor, or (kNonFiniteLevel) a non-finite solution
+    // value: locate the reference's zero pivot, if its order meets one
+    if (ctx->last.kind != 0)
+        return ctx->last.f32 ? diagnose_pivot<float>(ctx, row, level, err)
+                             : diagnose_pivot<double>(ctx, row, level, err);
+    if (level == tpb::kNonFiniteLevel) return TP_OK;  // the reference throws nothing either
     set_err(err, TP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(row), row, level);
     return TP_ERR_ZERO_PIVOT;
 }
@@ -569,8 +636,114 @@ tp_status solve_dev(tp_ctx* ctx, const T* sub, const T* diag, const T* super, co
     if (s != TP_OK) return s;
     bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, x, ctx->ws);
     const cudaStream_t st = pick_stream(ctx, stream);
+    ctx->last.kind = 1;
+    ctx->last.f32 = sizeof(T) == 4;
+    ctx->last.n = n;
+    ctx->last.sizes.assign(sizes, sizes + nsizes);
+    ctx->last.in[0] = sub;
+    ctx->last.in[1] = diag;
+    ctx->last.in[2] = super;
+    ctx->last.in[3] = rhs;
+    ctx->last.x = x;
     auto key = make_key<T>(1, n, sizes, nsizes, {sub, diag, super, rhs, x, ctx->ws});
     return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.solve(p); }, err);
+}
+
+// A solve reported a zero pivot (the device error word; dev_row / dev_level
+// are the device's own, in plan-level numbering). Locate it as the reference
+// would: replay detail::solve_partition_level's checks in ITS order with ITS
+// arithmetic (k_ref_sweep / k_ref_thomas, tp_split.cuh) — level by level,
+// block by block, up-sweep then down-sweep — on the level systems this solve
+// left in HBM (level 0 = the input, level l = the interface the device
+// assembled from level l-1). The first failing check gives ZeroPivotError's
+// row and the level whose system it indexes (0 = input; depth+1 = the
+// interface thomas_solve finishes). The reference's back_substitute pivots
+// are its up-sweep pivots, so Stage 3 never fails first. When no
+// reference-order check fails: a device pivot below the floor (the chunked
+// elimination met one the sequential sweeps do not) keeps the device's own
+// report; mere non-finite values return TP_OK, as the reference would.
+template <class T>
+tp_status diagnose_pivot(tp_ctx* ctx, int64_t dev_row, int32_t dev_level, tp_error* err) {
+    const auto& ls = ctx->last;
+    Plan<T> p;
+    const int32_t npol = ls.kind == 1 ? (int32_t)ls.sizes.size() : 0;
+    build_plan(ls.n, ls.sizes.data(), npol, p, true);
+    bind_plan(p, SysPtrs<T>{(const T*)ls.in[0], (const T*)ls.in[1], (const T*)ls.in[2], (const T*)ls.in[3]},
+              (T*)ls.x, ctx->ws);
+    const cudaStream_t st = ctx->own;
+    int64_t kmax = 1;
+    for (const auto& L : p.levels) kmax = std::max(kmax, L.K);
+    void* scratch = nullptr;
+    TP_CUDA(cudaMalloc(&scratch, (size_t)(kmax + 2) * sizeof(int64_t)));
+    int64_t* first = static_cast<int64_t*>(scratch);
+    unsigned long long* word = reinterpret_cast<unsigned long long*>(first + kmax);
+    auto fail = [&](int64_t row, int32_t level) {
+        cudaFree(scratch);
+        set_err(err, TP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(row), row, level);
+        return TP_ERR_ZERO_PIVOT;
+    };
+    auto thomas_row = [&](const SysPtrs<T>& sys, int64_t n, int64_t* row) -> cudaError_t {
+        cudaError_t e = tpb::launch_ref_thomas<T>(sys, n, first, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(row, first, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e;
+    };
+    SysPtrs<T> cur{(const T*)ls.in[0], (const T*)ls.in[1], (const T*)ls.in[2], (const T*)ls.in[3]};
+    int64_t cn = ls.n;
+    bool finished = false;  // a level below 4 rows ended the recursion (partition.hpp:197)
+    cudaError_t e = cudaSuccess;
+    int32_t l = 0;
+    for (; l < npol && e == cudaSuccess; ++l) {
+        int64_t row = -1;
+        if (cn < 4) {
+            e = thomas_row(cur, cn, &row);
+            if (e == cudaSuccess && row >= 0) return fail(row, l);
+            finished = true;
+            break;
+        }
+        const int64_t m = ls.sizes[(size_t)l];
+        const int64_t K = plan_blocks(cn, m);
+        unsigned long long jmin = ~0ULL;
+        e = cudaMemsetAsync(word, 0xFF, sizeof(unsigned long long), st);
+        if (e == cudaSuccess)
+            e = tpb::launch_ref_sweep<T>(cur, cn, m, K, first, word, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&jmin, word, sizeof(jmin), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess && jmin != ~0ULL) {
+            e = cudaMemcpy(&row, first + jmin, sizeof(int64_t), cudaMemcpyDeviceToHost);
+            if (e == cudaSuccess) return fail(row, l);
+        }
+        // the interface this policy level assembled: the next system
+        const Level<T>* lv = nullptr;
+        for (const auto& L : p.levels)
+            if (L.policy_level == l && !L.split) lv = &L;
+        if (lv == nullptr) break;
+        cur = SysPtrs<T>{lv->iface.sub, lv->iface.diag, lv->iface.sup, lv->iface.rhs};
+        cn = 2 * K;
+    }
+    if (e == cudaSuccess && !finished) {  // thomas_solve(iface) of the deepest level (:208-211), or of the input
+        int64_t row = -1;
+        e = thomas_row(cur, cn, &row);
+        if (e == cudaSuccess && row >= 0) return fail(row, npol);
+    }
+    cudaFree(scratch);
+    if (e != cudaSuccess) {
+        set_err(err, TP_ERR_CUDA, std::string("zero-pivot diagnosis: ") + cudaGetErrorString(e));
+        return TP_ERR_CUDA;
+    }
+    // no reference-order check fails. Only non-finite values (a singular
+    // system whose pivots stayed above the floor in both orders): the
+    // reference returns its x without an exception, so does this call.
+    if (dev_level == tpb::kNonFiniteLevel) return TP_OK;
+    // A device pivot below the floor: keep the device's report (a result
+    // computed through it is not returned), on the policy level its plan
+    // level belongs to
+    int32_t level = npol;
+    if (dev_level >= 0 && (size_t)dev_level < p.levels.size() && p.levels[(size_t)dev_level].policy_level >= 0)
+        level = p.levels[(size_t)dev_level].policy_level;
+    set_err(err, TP_ERR_ZERO_PIVOT,
+            "zero pivot at row " + std::to_string(dev_row) + " (device elimination order)", dev_row, level);
+    return TP_ERR_ZERO_PIVOT;
 }
 
 // H2D of the four arrays into the context's staging buffers, `body(device
@@ -651,10 +824,15 @@ tp_status solve_observe(tp_ctx* ctx, const T* sub, const T* diag, const T* super
                         void (*emit)(int64_t, int64_t, const T*, const T*, const T*, const T*, void*),
                         void* user, tp_error* err) {
     tp_status s = solve_host<T>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, err);
-    if (s != TP_OK || emit == nullptr) return s;
+    if (emit == nullptr || (s != TP_OK && s != TP_ERR_ZERO_PIVOT)) return s;
+    // the reference calls the observer after each level's assembly
+    // (partition.hpp:205-206): a zero pivot in level l's Stage 1 (or in the
+    // finishing thomas_solve, l = depth + 1) comes after levels 0 .. l-1
+    const int32_t upto = s == TP_OK ? nsizes : (err ? err->level : 0);
+    const tp_error saved = err ? *err : tp_error{};
     T* d[5];
-    s = ensure_dsys<T>(ctx, n, d, err);  // same buffers the solve used
-    if (s != TP_OK) return s;
+    tp_status s2 = ensure_dsys<T>(ctx, n, d, err);  // same buffers the solve used
+    if (s2 != TP_OK) return s2;
     Plan<T> p;
     build_plan(n, sizes, nsizes, p, true);
     bind_plan(p, SysPtrs<T>{d[0], d[1], d[2], d[3]}, d[4], ctx->ws);
@@ -662,15 +840,17 @@ tp_status solve_observe(tp_ctx* ctx, const T* sub, const T* diag, const T* super
     for (size_t l = 0; l < p.levels.size(); ++l) {
         const Level<T>& L = p.levels[l];
         if (L.internal) break;  // device-internal levels are not part of the policy
+        if (L.split || L.policy_level >= upto) continue;
         const int64_t n2 = 2 * L.K;
         h.resize((size_t)(4 * n2));
         TP_CUDA(cudaMemcpy(h.data(), L.iface.sub, n2 * sizeof(T), cudaMemcpyDeviceToHost));
         TP_CUDA(cudaMemcpy(h.data() + n2, L.iface.diag, n2 * sizeof(T), cudaMemcpyDeviceToHost));
         TP_CUDA(cudaMemcpy(h.data() + 2 * n2, L.iface.sup, n2 * sizeof(T), cudaMemcpyDeviceToHost));
         TP_CUDA(cudaMemcpy(h.data() + 3 * n2, L.iface.rhs, n2 * sizeof(T), cudaMemcpyDeviceToHost));
-        emit((int64_t)l, n2, h.data(), h.data() + n2, h.data() + 2 * n2, h.data() + 3 * n2, user);
+        emit((int64_t)L.policy_level, n2, h.data(), h.data() + n2, h.data() + 2 * n2, h.data() + 3 * n2, user);
     }
-    return TP_OK;
+    if (err) *err = saved;
+    return s;
 }
 
 // thomas_solve: no policy levels, only device-internal ones (large n) + finish.
@@ -696,6 +876,12 @@ tp_status thomas_host(tp_ctx* ctx, const T* sub, const T* diag, const T* super, 
             tp_status s2 = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
             if (s2 != TP_OK) return s2;
             bind_plan(p, SysPtrs<T>{d[0], d[1], d[2], d[3]}, d[4], ctx->ws);
+            ctx->last.kind = 2;
+            ctx->last.f32 = sizeof(T) == 4;
+            ctx->last.n = n;
+            ctx->last.sizes.clear();
+            for (int i = 0; i < 4; ++i) ctx->last.in[i] = d[i];
+            ctx->last.x = d[4];
             auto key = make_key<T>(2, n, nullptr, 0, {d[0], d[1], d[2], d[3], d[4], ctx->ws});
             return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.solve(p); }, err);
         },
@@ -704,14 +890,16 @@ tp_status thomas_host(tp_ctx* ctx, const T* sub, const T* diag, const T* super, 
 
 template <class T>
 tp_status residual_dev(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs, int64_t n,
-                       const T* x, double* out, tp_error* err) {
+                       const T* x, double* out, void* stream, tp_error* err) {
     clear_err(err);
     if (!ctx || !out || !sub || !diag || !super || !rhs || !x) {
         set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
         return TP_ERR_INVALID_ARGUMENT;
     }
     TP_CUDA(cudaSetDevice(ctx->device));
-    const cudaStream_t st = ctx->stream;
+    // on the caller's stream (NULL = the context's): ordered after the solve
+    // or generator that produced x on that stream
+    const cudaStream_t st = pick_stream(ctx, stream);
     TP_CUDA(cudaMemsetAsync(ctx->d_red, 0, 2 * sizeof(unsigned long long), st));
     TP_CUDA(tpb::launch_residual<T>(SysPtrs<T>{sub, diag, super, rhs}, n, x, ctx->d_red, ctx->sms, st));
     unsigned long long h[2];
@@ -747,6 +935,7 @@ tp_status shard_reduce(tp_ctx* ctx, const T* sub, const T* diag, const T* super,
     if (s != TP_OK) return s;
     bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, (T*)nullptr, ctx->ws);
     const cudaStream_t st = pick_stream(ctx, stream);
+    ctx->last.kind = 0;
     auto key = make_key<T>(3, n_local, sizes, nsizes, {sub, diag, super, rhs, eq8_dev, ctx->ws});
     return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.shard_reduce(p, eq8_dev); }, err);
 }
@@ -778,6 +967,7 @@ tp_status shard_finish(tp_ctx* ctx, const T* sub, const T* diag, const T* super,
     if (s != TP_OK) return s;
     bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, x_dev, ctx->ws);
     const cudaStream_t st = pick_stream(ctx, stream);
+    ctx->last.kind = 0;
     auto key = make_key<T>(4, n_local, sizes, nsizes,
                            {sub, diag, super, rhs, eq_all_dev, x_dev, ctx->ws},
                            ((int64_t)nranks << 32) | rank);
@@ -810,6 +1000,7 @@ tp_status shard_solve(tp_ctx* ctx, const T* sub, const T* diag, const T* super, 
     if (s != TP_OK) return s;
     bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, x_dev, ctx->ws);
     const cudaStream_t st = pick_stream(ctx, stream);
+    ctx->last.kind = 0;
     auto key = make_key<T>(5, n_local, sizes, nsizes, {sub, diag, super, rhs, x_dev, ctx->ws}, ctx->link_gen);
     return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.shard_solve(p); }, err);
 }
@@ -833,6 +1024,54 @@ tp_status generate_dev(tp_ctx* ctx, int64_t n, int64_t row0, int64_t n_global, u
     TP_CUDA(cudaSetDevice(ctx->device));
     TP_CUDA(tpb::launch_generate<T>(n, row0, n_global, seed, delta, sub, diag, super, rhs, ctx->sms,
                                     pick_stream(ctx, stream)));
+    return TP_OK;
+}
+
+// reduce_block(sys, Block{start, end}) — partition.hpp:77-126, on the device
+// with the reference's own arithmetic (k_ref_sweep<STORE>): the interface
+// pair and the up-sweep vectors of ReducedBlock (indexed by offset from
+// start; the entry at len-1 is left 0, as the reference never writes it).
+template <class T>
+tp_status reduce_block_host(tp_ctx* ctx, const T* sub, const T* diag, const T* super, const T* rhs, int64_t n,
+                            int64_t start, int64_t end, T* eq8, T* a, T* beta, T* gamma, T* delta,
+                            tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    if (!sub || !diag || !super || !rhs || !eq8) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "null argument");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    if (start < 0 || end > n || end - start < 2) {  // partition.hpp:79
+        set_err(err, TP_ERR_INVALID_SIZE, "block length must be >= 2");
+        return TP_ERR_INVALID_SIZE;
+    }
+    TP_CUDA(cudaSetDevice(ctx->device));
+    const int64_t len = end - start;
+    T* d[5];
+    tp_status s = ensure_dsys<T>(ctx, 2 * len + 8, d, err);  // 5 arrays of >= 2 len + 8 rows
+    if (s != TP_OK) return s;
+    const cudaStream_t st = ctx->stream;
+    const T* in[4] = {sub, diag, super, rhs};
+    for (int i = 0; i < 4; ++i)
+        TP_CUDA(cudaMemcpyAsync(d[i], in[i] + start, (size_t)len * sizeof(T), cudaMemcpyHostToDevice, st));
+    // outputs: d[4] = eq8 (8) + first (1 int64); up-sweep vectors in the
+    // second halves of d[0..3]
+    T* ov[4] = {d[0] + len, d[1] + len, d[2] + len, d[3] + len};
+    for (int i = 0; i < 4; ++i) TP_CUDA(cudaMemsetAsync(ov[i], 0, (size_t)len * sizeof(T), st));
+    int64_t* first = reinterpret_cast<int64_t*>(d[4] + 8);
+    TP_CUDA(tpb::launch_ref_sweep<T>(SysPtrs<T>{d[0], d[1], d[2], d[3]}, len, len, 1, first, nullptr, d[4], ov[0],
+                                     ov[1], ov[2], ov[3], st));
+    int64_t bad = -1;
+    TP_CUDA(cudaMemcpyAsync(&bad, first, sizeof(bad), cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaMemcpyAsync(eq8, d[4], 8 * sizeof(T), cudaMemcpyDeviceToHost, st));
+    T* outs[4] = {a, beta, gamma, delta};
+    for (int i = 0; i < 4; ++i)
+        if (outs[i]) TP_CUDA(cudaMemcpyAsync(outs[i], ov[i], (size_t)len * sizeof(T), cudaMemcpyDeviceToHost, st));
+    TP_CUDA(cudaStreamSynchronize(st));
+    if (bad >= 0) {
+        set_err(err, TP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(start + bad), start + bad, 0);
+        return TP_ERR_ZERO_PIVOT;
+    }
     return TP_OK;
 }
 
@@ -1007,13 +1246,25 @@ tp_status tp_thomas_solve_f32(tp_ctx* ctx, const float* sub, const float* diag, 
 }
 tp_status tp_residual_inf_f64_dev(tp_ctx* ctx, const double* sub, const double* diag,
                                   const double* super, const double* rhs, int64_t n,
-                                  const double* x, double* out, tp_error* err) {
-    return residual_dev<double>(ctx, sub, diag, super, rhs, n, x, out, err);
+                                  const double* x, double* out, void* stream, tp_error* err) {
+    return residual_dev<double>(ctx, sub, diag, super, rhs, n, x, out, stream, err);
 }
 tp_status tp_residual_inf_f32_dev(tp_ctx* ctx, const float* sub, const float* diag,
                                   const float* super, const float* rhs, int64_t n, const float* x,
-                                  double* out, tp_error* err) {
-    return residual_dev<float>(ctx, sub, diag, super, rhs, n, x, out, err);
+                                  double* out, void* stream, tp_error* err) {
+    return residual_dev<float>(ctx, sub, diag, super, rhs, n, x, out, stream, err);
+}
+
+// ---- reduce_block ---------------------------------------------------------
+tp_status tp_reduce_block_f64(tp_ctx* ctx, const double* sub, const double* diag, const double* super,
+                              const double* rhs, int64_t n, int64_t start, int64_t end, double* eq8,
+                              double* a, double* beta, double* gamma, double* delta, tp_error* err) {
+    return reduce_block_host<double>(ctx, sub, diag, super, rhs, n, start, end, eq8, a, beta, gamma, delta, err);
+}
+tp_status tp_reduce_block_f32(tp_ctx* ctx, const float* sub, const float* diag, const float* super,
+                              const float* rhs, int64_t n, int64_t start, int64_t end, float* eq8, float* a,
+                              float* beta, float* gamma, float* delta, tp_error* err) {
+    return reduce_block_host<float>(ctx, sub, diag, super, rhs, n, start, end, eq8, a, beta, gamma, delta, err);
 }
 
 // ---- sharded --------------------------------------------------------------
@@ -1189,7 +1440,7 @@ tp_status tp_plan_levels(int64_t n, const int64_t* sizes, int32_t nsizes, int64_
     }
     for (size_t l = 0; l < p.levels.size(); ++l) {
         if (level_n) level_n[l] = p.levels[l].n;
-        if (level_m) level_m[l] = p.levels[l].internal ? -p.levels[l].m : p.levels[l].m;
+        if (level_m) level_m[l] = (p.levels[l].internal || p.levels[l].split) ? -p.levels[l].m : p.levels[l].m;
     }
     if (nlevels) *nlevels = (int32_t)p.levels.size();
     if (n_final) *n_final = p.n_final;

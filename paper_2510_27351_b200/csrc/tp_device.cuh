@@ -114,6 +114,22 @@ __device__ __forceinline__ void report_pivot(unsigned long long* err, int level,
     }
 }
 
+// A solution value that is not finite: a singular system whose pivots the
+// device order never saw below the floor (the reference's order may have).
+// Reported with the lowest priority, so any pivot report wins.
+__device__ __forceinline__ void report_nonfinite(unsigned long long* err, int64_t row) {
+    if (err != nullptr)
+        atomicMin(err, (static_cast<unsigned long long>(kNonFiniteLevel) << 48) |
+                           (static_cast<unsigned long long>(row) & 0xFFFFFFFFFFFFULL));
+}
+template <class T, int L>
+__device__ __forceinline__ bool any_nonfinite(const T (&v)[L], int len = L) {
+    bool nf = false;
+#pragma unroll
+    for (int i = 0; i < L; ++i) nf |= (i < len) && !isfinite(v[i]);
+    return nf;
+}
+
 // ---------------------------------------------------------------------------
 // Leaf: one chunk held in registers sized L; its first K rows are valid
 // (K == L on the fixed-shape path; k_fast_rt dispatches on a runtime length).

@@ -134,7 +134,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
             T xv[L];
             lanes_tree_down<T, L, G>(s, c, xs, xe);
             leaf_expand<T, L, L>(s.r, s.rbeta, s.gam, s.del, xs, xe, xv);
-            if (active) store_rows<T, L, VEC>(x, row0, xv);  // pivots: checked by Stage 1
+            if (active) {
+                store_rows<T, L, VEC>(x, row0, xv);  // pivots: checked by Stage 1
+                if (any_nonfinite(xv)) report_nonfinite(err, row0);
+            }
         }
     }
 }
@@ -215,6 +218,7 @@ __global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
 #pragma unroll
                 for (int i = 0; i < LMAX; ++i)
                     if (i < len) x[row0 + i] = xv[i];
+                if (any_nonfinite(xv, len)) report_nonfinite(err, row0);
             }
         }
     }

@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
         if (tid == 0 && MODE == kSolve) {
             bad.see(sys.diag[0], 0);
             x[0] = sys.rhs[0] / sys.diag[0];
+            if (!isfinite(x[0])) report_nonfinite(err, 0);
         }
         report_pivot(err, level, bad.bad);
         return;
@@ -292,7 +293,12 @@ __global__ void __launch_bounds__(kFinalThreads2) k_final(SysPtrs<T> sys, int64_
     TP_TRACE(9);
     __syncthreads();
     TP_TRACE(10);
-    for (int64_t i = tid; i < n; i += kFinalThreads2) x[i] = sa[i];
+    bool nf = false;
+    for (int64_t i = tid; i < n; i += kFinalThreads2) {
+        x[i] = sa[i];
+        nf |= !isfinite(sa[i]);
+    }
+    if (nf) report_nonfinite(err, 0);
     TP_TRACE(11);
     TP_TRACE_FLUSH;
     report_pivot(err, level, bad.bad);
@@ -518,6 +524,7 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             if (i < len) xdst[grow - xbase + i] = xv[i];
+        if (any_nonfinite(xv, len)) report_nonfinite(err, grow);
     }
     TP_TRACE(9);
     TP_TRACE(10);
@@ -742,7 +749,13 @@ __global__ void __launch_bounds__(kFinNT, 1)
     TP_LF_TRACE(4);
     {
         LfSlots w(tid, m, nb, S);
-        for (int e = tid; e < rows; e += kFinNT, w.next()) x[r0 + e] = la[w.slot()];
+        bool nf = false;
+        for (int e = tid; e < rows; e += kFinNT, w.next()) {
+            const T v = la[w.slot()];
+            x[r0 + e] = v;
+            nf |= !isfinite(v);
+        }
+        if (nf) report_nonfinite(err, r0);
     }
     TP_LF_TRACE(5);
     report_pivot(err, level, bad_lv.bad);

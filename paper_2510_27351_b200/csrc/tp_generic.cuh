@@ -205,7 +205,13 @@ __global__ void __launch_bounds__(kFinalThreads) k_generic(SysPtrs<T> sys, int64
                 if (len > 1) a[len - 1] = xe;
             }
             __syncthreads();
-            for (int64_t i = tid; i < trows; i += NT) x[trow0 + i] = s.a[i];
+            bool nf = false;
+            for (int64_t i = tid; i < trows; i += NT) {
+                const T v = s.a[i];
+                x[trow0 + i] = v;
+                nf |= !isfinite(v);
+            }
+            if (nf) report_nonfinite(err, trow0);
         }
         __syncthreads();
         (void)lane;

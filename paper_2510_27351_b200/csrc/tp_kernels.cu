@@ -43,6 +43,7 @@ __device__ unsigned long long g_trace[24];  // [0, 12) finishing solve, [12, 18)
 #include "tp_generic.cuh"
 #include "tp_final.cuh"
 #include "tp_fold.cuh"
+#include "tp_split.cuh"
 
 namespace tpb {
 
@@ -488,6 +489,42 @@ cudaError_t init_kernel_attributes() {
 }
 
 template <class T>
+cudaError_t launch_split(int mode, const SysPtrs<T>& sys, int64_t row_base, int64_t nblocks, int64_t blen,
+                         int64_t nsub, int64_t q_base, const IfacePtrs<T>& out, const T* xi, T* x,
+                         unsigned long long* err, int level, cudaStream_t st) {
+    if (nblocks < 1 || nsub < 1 || blen < 2 * nsub || (blen + nsub - 1) / nsub > kSplitRows)
+        return cudaErrorInvalidValue;
+    const int64_t grid = (nblocks * nsub + 127) / 128;
+    if (mode == kStage1)
+        return launch_k(level, k_split<T, kStage1>, (unsigned)grid, 128, 0, st, sys, row_base, nblocks, blen, nsub,
+                        q_base, out, xi, x, err, level);
+    return launch_k(level, k_split<T, kStage3>, (unsigned)grid, 128, 0, st, sys, row_base, nblocks, blen, nsub,
+                    q_base, out, xi, x, err, level);
+}
+
+template <class T>
+cudaError_t launch_ref_sweep(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, int64_t* first,
+                             unsigned long long* jmin, T* eq8, T* ua, T* ubeta, T* ugamma, T* udelta,
+                             cudaStream_t st) {
+    int64_t grid = (K + 127) / 128;
+    if (grid > 148 * 16) grid = 148 * 16;
+    if (grid < 1) grid = 1;
+    if (eq8 != nullptr)
+        k_ref_sweep<T, true><<<(unsigned)grid, 128, 0, st>>>(sys, n, m, K, first, jmin, eq8, ua, ubeta, ugamma,
+                                                             udelta);
+    else
+        k_ref_sweep<T, false><<<(unsigned)grid, 128, 0, st>>>(sys, n, m, K, first, jmin, nullptr, nullptr, nullptr,
+                                                              nullptr, nullptr);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_ref_thomas(const SysPtrs<T>& sys, int64_t n, int64_t* out, cudaStream_t st) {
+    k_ref_thomas<T><<<1, 32, 0, st>>>(sys, n, out);
+    return cudaGetLastError();
+}
+
+template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st) {
     return launch_k(level, k_gather_solve<T>, 1, 32, 0, st, eqs, nranks, rank, x2, scratch, err, level);
@@ -533,6 +570,12 @@ cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsign
     template cudaError_t launch_level_final<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t,        \
                                                const IfacePtrs<T>&, T*,                             \
                                                unsigned long long*, int, cudaStream_t);             \
+    template cudaError_t launch_split<T>(int, const SysPtrs<T>&, int64_t, int64_t, int64_t, int64_t,   \
+                                         int64_t, const IfacePtrs<T>&, const T*, T*,                \
+                                         unsigned long long*, int, cudaStream_t);                   \
+    template cudaError_t launch_ref_sweep<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t, int64_t*,   \
+                                             unsigned long long*, T*, T*, T*, T*, T*, cudaStream_t);  \
+    template cudaError_t launch_ref_thomas<T>(const SysPtrs<T>&, int64_t, int64_t*, cudaStream_t);      \
     template cudaError_t launch_gather_solve<T>(const T*, int, int, T*, T*, unsigned long long*,    \
                                                 int, cudaStream_t);                                 \
     template cudaError_t launch_generate<T>(int64_t, int64_t, int64_t, uint64_t, double, T*, T*,    \

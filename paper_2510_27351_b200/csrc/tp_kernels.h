@@ -22,6 +22,10 @@ constexpr int kFinalThreads2 = 512;   // k_final CTA
 // (32 B per FP64 row; 6144 rows = 192 KiB of the 227 KiB opt-in limit).
 constexpr int64_t kFinalCap = 6144;
 constexpr size_t kMaxDynSmem = 227 * 1024;
+// Long-block path (k_split, tp_split.cuh): blocks longer than kSplitAbove rows
+// are cut into chunks of <= kSplitRows rows by a split level.
+constexpr int kSplitRows = 8;
+constexpr int64_t kSplitAbove = 2048;
 constexpr unsigned long long kNoError = ~0ULL;
 
 template <class T>
@@ -48,6 +52,9 @@ struct IfacePtrs {
 constexpr int kMaxPeers = 64;
 constexpr int kMailboxEntryDoubles = 16;
 constexpr int kExchangeLevel = 0x7FFF;  // err-word level of a peer-exchange timeout
+// err-word level of a non-finite solution value (no pivot below the floor
+// seen): the host then replays the reference's pivot order (diagnose_pivot)
+constexpr int kNonFiniteLevel = 0x7FFE;
 struct ShardLink {
     double* peers[kMaxPeers];   // every rank's mailbox, by rank (peers[rank] = own)
     double* own;                // this rank's mailbox
@@ -96,6 +103,22 @@ bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem);
 template <class T>
 cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, const IfacePtrs<T>& iface,
                                T* x, unsigned long long* err, int level, cudaStream_t st);
+// One split level (tp_split.cuh): nblocks blocks of blen rows starting at
+// row_base, nsub chunks each, chunk pairs written from pair q_base on.
+template <class T>
+cudaError_t launch_split(int mode, const SysPtrs<T>& sys, int64_t row_base, int64_t nblocks, int64_t blen,
+                         int64_t nsub, int64_t q_base, const IfacePtrs<T>& out, const T* xi, T* x,
+                         unsigned long long* err, int level, cudaStream_t st);
+// Reference-order sweeps (tp_split.cuh): reduce_block over make_plan(n, m)
+// (first[j] = the block's failing pivot row or -1; jmin = atomicMin of the
+// failing block indices; with eq8 != NULL the interface pairs and up-sweep
+// vectors are stored) and thomas_solve's pivot scan.
+template <class T>
+cudaError_t launch_ref_sweep(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, int64_t* first,
+                             unsigned long long* jmin, T* eq8, T* ua, T* ubeta, T* ugamma, T* udelta,
+                             cudaStream_t st);
+template <class T>
+cudaError_t launch_ref_thomas(const SysPtrs<T>& sys, int64_t n, int64_t* out, cudaStream_t st);
 template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st);

@@ -244,6 +244,7 @@ tp_status tp_obs_read(const char* path, tp_obs_set** out, int64_t* count, tp_err
     };
     auto bad = [&](size_t ln, const std::string& what) {
         set_err(err, TP_ERR_BAD_NUMBER, "line " + std::to_string(ln) + ": bad number: " + what);
+        if (err) err->row = (int64_t)ln;
         return TP_ERR_BAD_NUMBER;
     };
     auto parse_i64 = [](const std::string& s, int64_t& v) {
@@ -279,6 +280,7 @@ tp_status tp_obs_read(const char* path, tp_obs_set** out, int64_t* count, tp_err
             set_err(err, TP_ERR_BAD_NUMBER,
                     "line " + std::to_string(ln) + ": bad number: expected 9 fields, got " +
                         std::to_string(f.size()));
+            if (err) err->row = (int64_t)ln;
             return TP_ERR_BAD_NUMBER;
         }
         int64_t n;
@@ -315,6 +317,7 @@ tp_status tp_obs_read(const char* path, tp_obs_set** out, int64_t* count, tp_err
             } else {
                 set_err(err, TP_ERR_BAD_NUMBER,
                         "line " + std::to_string(ln) + ": bad number: optimum row carries neither m nor opt_R");
+                if (err) err->row = (int64_t)ln;
                 return TP_ERR_BAD_NUMBER;
             }
             if (!f[7].empty()) {

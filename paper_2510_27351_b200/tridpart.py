@@ -230,10 +230,19 @@ class TridiagonalSystem:
             return bool(torch.all(self.diag.abs() > self.sub.abs() + self.super.abs()))
         return bool(np.all(np.abs(self.diag) > np.abs(self.sub) + np.abs(self.super)))
 
+    def check_shape(self):
+        """sub, super and rhs must have diag's length: the C-ABI reads n
+        elements of each (the reference indexes them up to size())."""
+        n = self.size()
+        if any(int(v.shape[0]) != n for v in (self.sub, self.super, self.rhs)):
+            raise InvalidSizeError("sub, diag, super and rhs must have the same length")
+
     def _host_ptrs(self):
+        self.check_shape()
         return [C.c_void_p(a.ctypes.data) for a in (self.sub, self.diag, self.super, self.rhs)]
 
     def _dev_ptrs(self):
+        self.check_shape()
         want = str(self.diag.dtype)
         for a in (self.sub, self.diag, self.super, self.rhs):
             if not (a.is_cuda and a.is_contiguous()) or str(a.dtype) != want or \
@@ -248,10 +257,25 @@ Tridiagonal = TridiagonalSystem
 
 def generate_system(n: int, seed: int, delta: float = 1.5, device: bool = False,
                     row0: int = 0, n_global: Optional[int] = None, dtype: str = "float64"):
-    """Synthetic strictly dominant system with the distributions of
-    generate_system (bench.hpp:68-93), generated ON THE DEVICE from a
-    counter-based hash (not bit-identical to std::mt19937_64). Returns device
-    tensors when ``device`` else host copies."""
+    """generate_system (bench.hpp:68-93).
+
+    Host (``device=False``, the default): BIT-IDENTICAL to the reference — the
+    library's C++ generator (``tp_generate_system_f64``) runs std::mt19937_64(seed)
+    with libstdc++'s uniform_real_distribution / bernoulli_distribution in the
+    reference's draw order. Whole float64 systems only.
+
+    ``device=True``: generated ON THE DEVICE from a counter-based hash with the
+    same distributions (NOT bit-identical; throughput runs), returned as CUDA
+    tensors; ``row0`` / ``n_global`` select one shard's slice of a global
+    system and ``dtype`` may be float32."""
+    if not device:
+        if row0 != 0 or n_global not in (None, n) or dtype not in ("float64", "f64", np.float64):
+            raise ValueError("the bit-identical host generator builds whole float64 systems; "
+                             "use device=True for shard slices or float32")
+        arrs = [np.empty(max(int(n), 0), dtype=np.float64) for _ in range(4)]
+        _call(lib.tp_generate_system_f64, int(n), C.c_uint64(seed), float(delta),
+              *[C.c_void_p(a.ctypes.data) for a in arrs])
+        return TridiagonalSystem(*arrs)
     import torch
 
     n_global = n if n_global is None else n_global
@@ -262,9 +286,7 @@ def generate_system(n: int, seed: int, delta: float = 1.5, device: bool = False,
     fn = lib.tp_generate_system_f32_dev if tdt == torch.float32 else lib.tp_generate_system_f64_dev
     _call(fn, ctx.handle, n, row0, n_global, C.c_uint64(seed), delta,
           *[C.c_void_p(a.data_ptr()) for a in arrs], C.c_void_p(stream))
-    if device:
-        return TridiagonalSystem(*arrs)
-    return TridiagonalSystem(*[a.cpu().numpy() for a in arrs])
+    return TridiagonalSystem(*arrs)
 
 
 def residual_inf(sys: TridiagonalSystem, x) -> float:
@@ -273,8 +295,11 @@ def residual_inf(sys: TridiagonalSystem, x) -> float:
         ctx = context()
         out = C.c_double()
         fn = lib.tp_residual_inf_f32_dev if sys.is_f32 else lib.tp_residual_inf_f64_dev
+        if not (x.is_cuda and x.is_contiguous() and x.dtype == sys.diag.dtype and
+                int(x.shape[0]) == sys.size()):
+            raise ValueError("x must be a contiguous CUDA tensor of the system's dtype and size")
         _call(fn, ctx.handle, *sys._dev_ptrs(), sys.size(),
-              C.c_void_p(x.data_ptr()), C.byref(out))
+              C.c_void_p(x.data_ptr()), C.byref(out), C.c_void_p(torch_stream()))
         return float(out.value)
     x = np.asarray(x, dtype=sys.diag.dtype)
     ax = sys.diag * x
@@ -320,6 +345,68 @@ def make_plan(n: int, m: int) -> PartitionPlan:
     b = np.empty(k.value + 1, dtype=np.int64)
     _call(lib.tp_make_plan, n, m, b.ctypes.data_as(_I64), C.byref(k))
     return PartitionPlan(n, m, [Block(int(b[j]), int(b[j + 1])) for j in range(k.value)])
+
+
+@dataclass
+class ReducedBlock:
+    """partition.hpp:52-71: eq1 / eq2 of a block plus its up-sweep vectors
+    (indexed by offset from ``start``; the entry at len-1 is unused)."""
+    start: int = 0
+    end: int = 0
+    alpha1: float = 0.0
+    beta1: float = 0.0
+    gamma1: float = 0.0
+    delta1: float = 0.0
+    alpha2: float = 0.0
+    beta2: float = 0.0
+    gamma2: float = 0.0
+    delta2: float = 0.0
+    a: np.ndarray = None
+    beta: np.ndarray = None
+    gamma: np.ndarray = None
+    delta: np.ndarray = None
+
+
+def reduce_block(sys: TridiagonalSystem, blk: Block) -> ReducedBlock:
+    """reduce_block (partition.hpp:77-126), on the device with the reference's
+    own sequential arithmetic (tp_reduce_block_*)."""
+    start, end = int(blk.start), int(blk.end)
+    ln = end - start
+    if ln < 2 or end > sys.size() or start < 0:
+        raise InvalidSizeError("block length must be >= 2")
+    dt = np.float32 if sys.is_f32 else np.float64
+    eq = np.empty(8, dtype=dt)
+    vec = [np.zeros(ln, dtype=dt) for _ in range(4)]
+    fn = lib.tp_reduce_block_f32 if sys.is_f32 else lib.tp_reduce_block_f64
+    _call(fn, context().handle, *sys._host_ptrs(), sys.size(), start, end, C.c_void_p(eq.ctypes.data),
+          *[C.c_void_p(v.ctypes.data) for v in vec])
+    return ReducedBlock(start, end, *[float(v) for v in eq], *vec)
+
+
+def assemble_interface(blocks: Sequence[ReducedBlock]) -> TridiagonalSystem:
+    """assemble_interface (partition.hpp:131-151): rows 2j / 2j+1 = eq1 / eq2 of block j."""
+    k = len(blocks)
+    out = [np.empty(2 * k) for _ in range(4)]
+    for j, b in enumerate(blocks):
+        for arr, (v1, v2) in zip(out, ((b.alpha1, b.alpha2), (b.beta1, b.beta2),
+                                       (b.gamma1, b.gamma2), (b.delta1, b.delta2))):
+            arr[2 * j], arr[2 * j + 1] = v1, v2
+    return TridiagonalSystem(*out)
+
+
+def back_substitute(blk: ReducedBlock, x_s: float, x_e: float) -> np.ndarray:
+    """back_substitute (partition.hpp:156-172): x_{s+1} .. x_{e-1} from the
+    stored up-sweep rows, left to right."""
+    ln = blk.end - blk.start
+    out = np.empty(max(ln - 2, 0))
+    prev = x_s
+    for k in range(1, ln - 1):
+        piv = blk.beta[k]
+        if abs(piv) < kPivotFloor:
+            raise ZeroPivotError(blk.start + k)
+        prev = (blk.delta[k] - blk.a[k] * prev - blk.gamma[k] * x_e) / piv
+        out[k - 1] = prev
+    return out
 
 
 class RecursionPolicy:
@@ -394,6 +481,10 @@ def solve_partition_async(sys: TridiagonalSystem, policy, out=None):
     sz = _policy_array(policy)
     ctx = context()
     n = sys.size()
+    if out is not None and not (out.is_cuda and out.is_contiguous() and out.dtype == sys.diag.dtype and
+                                out.device == sys.diag.device and int(out.shape[0]) >= n):
+        raise ValueError("out must be a contiguous CUDA tensor of the system's dtype and device, "
+                         "with at least n elements")
     x = out if out is not None else torch.empty(n, dtype=sys.diag.dtype, device=sys.diag.device)
     stream = torch_stream()
     fn = lib.tp_solve_partition_f32_dev if sys.is_f32 else lib.tp_solve_partition_f64_dev

@@ -45,7 +45,7 @@ def test_library_is_sm100a_only(tp):
 def test_abi_version(tp):
     from paper_2510_27351_b200 import _lib
 
-    assert _lib.lib.tp_abi_version() == 1
+    assert _lib.lib.tp_abi_version() == 2
 
 
 def test_context_without_gpu_fails_loudly(tp):
@@ -226,3 +226,98 @@ def test_shard_entries_reject_bad_arguments_without_a_device(tp):
     with pytest.raises(ValueError):
         from paper_2510_27351_b200.tridpart import _call
         _call(lib.tp_shard_mailbox, None, 0, C.byref(box))
+
+
+# ------------------------------------------------------- round 2: host pieces
+def test_generate_system_is_bit_identical_to_the_reference(tp, oracle_mod):
+    """generate_system (bench.hpp:68-93): the library's host generator equals the
+    reference's own (oracle/_ref, the unmodified headers) bit for bit."""
+    if not oracle_mod.ref_available():
+        pytest.skip("oracle/_ref not built")
+    for n, seed, delta in ((2, 0, 1.5), (3, 1, 1.5), (16, 1, 1.5), (10_000, 1, 1.5),
+                           (100_001, 20240601, 2.5), (1_000_000, 1, 1.5)):
+        s = tp.generate_system(n, seed, delta)
+        r = oracle_mod.generate_system(n, seed, delta, impl="ref")
+        for got, want in ((s.sub, r.sub), (s.diag, r.diag), (s.super, r.sup), (s.rhs, r.rhs)):
+            assert got.tobytes() == want.tobytes(), (n, seed)
+    with pytest.raises(tp.InvalidSizeError):
+        tp.generate_system(1, 0)
+    with pytest.raises(tp.InvalidSizeError):
+        tp.generate_system(10, 0, delta=1.0)
+
+
+def test_generate_system_golden_sums(tp):
+    """SURVEY §8(c) pins of generate_system(N, 1) (reference-generated)."""
+    s = tp.generate_system(10_000, 1)
+    assert abs(float(np.sum(s.diag)) - 10.578227862787433) < 1e-9
+    assert abs(float(np.sum(s.rhs)) - -26.256125191010906) < 1e-9
+
+
+def _levels(tp, n, sizes):
+    return tp.plan_levels(n, tp.RecursionPolicy(sizes))
+
+
+@pytest.mark.parametrize("n,m", [(10_000, 2049), (10_000, 4096), (100_000, 10_000), (1_000_000, 100_000),
+                                 (100_000, 100_000), (100_000, 250_000), (5_000, 4_999), (20_001, 10_000)])
+def test_long_blocks_become_split_chains(tp, n, m):
+    """Blocks longer than 2048 rows are reduced through split levels (negative m
+    in plan_levels) ending in a level with the original block count: the
+    interface handed on is 2K rows, K = make_plan(n, m)'s block count."""
+    ln, lm, nf = _levels(tp, n, [m])
+    k = len(tp.make_plan(n, m).blocks)
+    assert lm[0] < 0, (ln, lm)                  # the first plan level is a split
+    policy = [i for i, v in enumerate(lm) if v > 0]
+    assert policy, (ln, lm)
+    last = policy[0]                            # the level keeping the block boundaries
+    assert all(v < 0 for v in lm[:last])
+    # each split level's system shrinks ~4x (chunks of <= 8 rows -> 2 rows)
+    for a, b in zip(ln[:last], ln[1:last + 1]):
+        assert b <= a // 3 + 2
+    # what follows the policy level is the 2K-row interface (or device-internal levels of it)
+    if last + 1 < len(ln):
+        assert ln[last + 1] == 2 * k
+    else:
+        assert nf == 2 * k
+
+
+def test_short_blocks_are_not_split(tp):
+    for m in (2, 4, 64, 256, 1250, 2048):
+        _, lm, _ = _levels(tp, 100_000, [m])
+        assert lm[0] == m
+
+
+def test_cpp_drop_in_headers_compile_standalone(tmp_path):
+    """Every shadow header under include/tridpart compiles on its own (the
+    reference's include layout: a caller swaps only its -I path)."""
+    hdrs = sorted(os.listdir(os.path.join(ROOT, "include", "tridpart")))
+    assert {"bench.hpp", "errors.hpp", "io.hpp", "knn.hpp", "observations.hpp", "partition.hpp",
+            "policy.hpp", "tridiagonal.hpp"} <= set(hdrs)
+    for h in hdrs:
+        src = tmp_path / f"inc_{h}.cpp"
+        src.write_text(f'#include "tridpart/{h}"\nint main() {{ return 0; }}\n')
+        r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), str(src)],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, (h, r.stderr)
+
+
+def test_reference_unit_tests_build_against_the_drop_in_headers(tmp_path):
+    """The reference's unmodified proj/tests/test_{partition,tridiagonal,policy}.cpp
+    build with -I<repo>/include in place of -I<reference>/proj/include (built by
+    tests/cpp/Makefile; run on the GPU in test_cpp_shim.py)."""
+    exe = os.path.join(ROOT, "tests", "cpp", "_build", "ref_unit_tests")
+    if not os.path.exists("/root/reference/proj/tests/test_partition.cpp"):
+        if not os.path.exists(exe):
+            pytest.skip("no reference checkout and no prebuilt binary")
+        return
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert os.path.exists(exe)
+    # the reference's include tree must not be on the path: every tridpart/ header
+    # the objects saw is ours
+    dep = subprocess.run(["g++", "-std=c++20", "-M", "-I", os.path.join(ROOT, "include"),
+                          "-I", os.path.join(ROOT, "tests", "cpp", "catch_shim"),
+                          "-I", "/root/reference/proj/tests", "-DTRIDPART_DATA_DIR=\"x\"",
+                          "/root/reference/proj/tests/test_partition.cpp"], capture_output=True, text=True)
+    assert dep.returncode == 0, dep.stderr
+    assert "/root/reference/proj/include" not in dep.stdout
+    assert os.path.join(ROOT, "include", "tridpart", "partition.hpp") in dep.stdout
