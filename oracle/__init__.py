@@ -95,6 +95,10 @@ def ref():
         lib.ref_system_new.argtypes = [C.c_int64, _D, _D, _D, _D]
         lib.ref_system_generate.restype = C.c_void_p
         lib.ref_system_generate.argtypes = [C.c_int64, C.c_uint64]
+        lib.ref_system_view.restype = None
+        lib.ref_system_view.argtypes = [C.c_void_p] + [C.POINTER(_D)] * 4
+        lib.ref_system_thomas.restype = C.c_int64
+        lib.ref_system_thomas.argtypes = [C.c_void_p, _D]
         lib.ref_system_free.restype = None
         lib.ref_system_free.argtypes = [C.c_void_p]
         lib.ref_system_solve.restype = C.c_int64
@@ -148,6 +152,42 @@ class System:
 
     def ptrs(self):
         return _dp(self.sub), _dp(self.diag), _dp(self.sup), _dp(self.rhs)
+
+
+class RefSystem:
+    """A system owned by the reference library (oracle/_ref): generated there
+    by its own generate_system, solved there without copying the arrays;
+    ``view()`` exposes the arrays as numpy views (no copy). For N = 1e9."""
+
+    def __init__(self, n: int, seed: int):
+        self.n = n
+        self.h = ref().ref_system_generate(n, seed)
+        if not self.h:
+            raise MemoryError("ref_system_generate failed")
+
+    def view(self) -> System:
+        ps = [_D() for _ in range(4)]
+        ref().ref_system_view(self.h, *[C.byref(p) for p in ps])
+        arrs = [np.ctypeslib.as_array(p, (self.n,)) for p in ps]
+        v = System.__new__(System)
+        v.sub, v.diag, v.sup, v.rhs = arrs
+        return v
+
+    def solve(self, sizes) -> np.ndarray:
+        x = np.empty(self.n)
+        sz = np.asarray(sizes, dtype=np.int64)
+        _status(ref().ref_system_solve(self.h, sz.ctypes.data_as(_I64), len(sz), _dp(x)))
+        return x
+
+    def thomas(self) -> np.ndarray:
+        x = np.empty(self.n)
+        _status(ref().ref_system_thomas(self.h, _dp(x)))
+        return x
+
+    def free(self):
+        if self.h:
+            ref().ref_system_free(self.h)
+            self.h = None
 
 
 def generate_system(n: int, seed: int, delta: float = 1.5, impl: str = "port") -> System:

@@ -80,6 +80,22 @@ void* ref_system_generate(int64_t n, uint64_t seed) {
 }
 void ref_system_free(void* h) { delete static_cast<Tridiagonal*>(h); }
 
+// Pointers to a handle's own arrays (so callers view them without a copy).
+void ref_system_view(void* h, double** a, double** b, double** c, double** d) {
+    auto& s = *static_cast<Tridiagonal*>(h);
+    *a = s.sub.data();
+    *b = s.diag.data();
+    *c = s.super.data();
+    *d = s.rhs.data();
+}
+
+int64_t ref_system_thomas(void* h, double* x) {
+    return guarded([&] {
+        const auto r = thomas_solve(*static_cast<Tridiagonal*>(h));
+        std::memcpy(x, r.data(), r.size() * sizeof(double));
+    });
+}
+
 int64_t ref_system_solve(void* h, const int64_t* sizes, int32_t nsizes, double* x) {
     return guarded([&] {
         RecursionPolicy p;

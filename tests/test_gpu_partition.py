@@ -285,11 +285,38 @@ def test_reciprocal_is_within_one_ulp(tp):
 
 
 
-@pytest.mark.skipif(os.environ.get("TPB_SLOW") != "1", reason="set TPB_SLOW=1 (needs ~130 GB host RAM)")
+def _host_ram_gb() -> float:
+    try:
+        import psutil
+
+        return psutil.virtual_memory().available / 2**30
+    except Exception:
+        return 0.0
+
+
+def _floored_stats(x, ref, floor=1e-6, chunk=50_000_000):
+    """max_i |x_i - ref_i| / max(|ref_i|, floor), chunked (N = 1e9), with where it occurs."""
+    worst, at = -1.0, 0
+    for lo in range(0, ref.size, chunk):
+        d = np.abs(x[lo:lo + chunk] - ref[lo:lo + chunk]) / np.maximum(np.abs(ref[lo:lo + chunk]), floor)
+        i = int(np.argmax(d))
+        if d[i] > worst:
+            worst, at = float(d[i]), lo + i
+    return {"floored_rel": worst, "at_row": at, "abs_diff": float(abs(x[at] - ref[at])),
+            "abs_ref": float(abs(ref[at]))}
+
+
+@pytest.mark.skipif(_host_ram_gb() < 140, reason="config 4 at full size needs ~140 GB of free host RAM")
 def test_config4_n1e9_against_the_reference_itself(tp, oracle_mod):
     """Config 4 at full size: the reference's own generator and solver
-    (oracle/_ref) at N = 1e9 with the kNN policy of the global N, against the
-    single-GPU solve and the 8-rank sharded algorithm (simulated ranks)."""
+    (oracle/_ref: the system lives in the reference library, solved there
+    without copies) at N = 1e9 with the kNN policy of the global N, against the
+    single-GPU solve and the 8-rank sharded algorithm (simulated ranks).
+
+    The floored elementwise metric sits at the FP64 noise floor
+    here: rows with |x| ~ 1e-6 come out of O(1) cancellations, so any two exact
+    algorithms differ there by ~1e-16 absolute. The reference's own partition
+    solve against its own Thomas is recorded beside ours as that floor."""
     import json
     import time
 
@@ -298,25 +325,37 @@ def test_config4_n1e9_against_the_reference_itself(tp, oracle_mod):
     n = 1_000_000_000
     pol = tp.predicted_policy(n)
     assert pol.sizes == [64, 10, 32, 32]
+    out = {"n": n, "policy": pol.sizes, "host_ram_gb": _host_ram_gb()}
     t0 = time.time()
-    s = oracle_mod.generate_system(n, 1, impl="ref")
-    t_gen = time.time() - t0
-    t0 = time.time()
-    ref = oracle_mod.solve_partition(s, pol.sizes, impl="ref")
-    t_ref = time.time() - t0
-    x = tp.solve_partition(_sys(tp, s), pol)
-    out = {"n": n, "policy": pol.sizes, "ref_generate_s": t_gen, "ref_solve_s": t_ref,
-           "single_gpu": {"rel_inf_diff": oracle_mod.rel_inf_diff(x, ref),
-                          "floored_rel": oracle_mod.floored_rel_diff(x, ref),
-                          "residual": oracle_mod.residual_inf(s, x)}}
-    del x
-    xs = sharded.simulate_ranks(s.sub, s.diag, s.sup, s.rhs, 8, pol.sizes)
-    out["sharded_8_ranks"] = {"rel_inf_diff": oracle_mod.rel_inf_diff(xs, ref),
-                              "floored_rel": oracle_mod.floored_rel_diff(xs, ref),
-                              "residual": oracle_mod.residual_inf(s, xs)}
+    rs = oracle_mod.RefSystem(n, 1)
+    out["ref_generate_s"] = time.time() - t0
+    try:
+        s = rs.view()
+        t0 = time.time()
+        ref = rs.solve(pol.sizes)
+        out["ref_solve_s"] = time.time() - t0
+        t0 = time.time()
+        x = tp.solve_partition(_sys(tp, s), pol)
+        out["gpu_host_call_s"] = time.time() - t0
+        out["single_gpu"] = {"rel_inf_diff": oracle_mod.rel_inf_diff(x, ref), **_floored_stats(x, ref),
+                             "residual": oracle_mod.residual_inf(s, x)}
+        del x
+        xs = sharded.simulate_ranks(s.sub, s.diag, s.sup, s.rhs, 8, pol.sizes)
+        out["sharded_8_ranks"] = {"rel_inf_diff": oracle_mod.rel_inf_diff(xs, ref), **_floored_stats(xs, ref),
+                                  "residual": oracle_mod.residual_inf(s, xs)}
+        del xs
+        t0 = time.time()
+        th = rs.thomas()
+        out["ref_thomas_s"] = time.time() - t0
+        out["reference_partition_vs_its_thomas"] = {"rel_inf_diff": oracle_mod.rel_inf_diff(ref, th),
+                                                    **_floored_stats(ref, th)}
+        del th
+    finally:
+        rs.free()
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/parity_n1e9.json", "w") as f:
         json.dump(out, f, indent=1)
+    print(json.dumps(out))
     for k in ("single_gpu", "sharded_8_ranks"):
         assert out[k]["rel_inf_diff"] <= TOL_NORM
         assert out[k]["floored_rel"] <= TOL_FLOOR
@@ -430,15 +469,15 @@ def test_randomized_sizes_and_policies_against_the_oracle(tp, oracle_mod):
         assert np.all(np.isfinite(x)) and d <= TOL_NORM and r <= TOL_RES, (case, n, sizes, d, r)
 
 
-@pytest.mark.skipif(os.environ.get("TPB_SLOW") != "1", reason="set TPB_SLOW=1 (a few minutes)")
 def test_randomized_large_sizes_and_deep_policies(tp, oracle_mod):
-    """60 random (N, policy) pairs with N log-uniform in [4e5, 2e7], depth
-    0..4, m in [2, 400], against the oracle (all three parity gates)."""
+    """30 random (N, policy) pairs with N log-uniform in [4e5, 2e7], depth
+    0..4, m log-uniform in [2, 20000] (long blocks included), against the
+    oracle (all three parity gates)."""
     rng = np.random.default_rng(99)
-    for case in range(60):
+    for case in range(30):
         n = int(np.exp(rng.uniform(np.log(4e5), np.log(2e7))))
         depth = int(rng.integers(0, 5))
-        sizes = [int(rng.integers(2, 400)) for _ in range(depth + 1)]
+        sizes = [int(np.exp(rng.uniform(np.log(2), np.log(20_000)))) for _ in range(depth + 1)]
         s = oracle_mod.generate_system(n, 50_000 + case)
         _check(oracle_mod, s, tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes)),
                oracle_mod.solve_partition(s, sizes))
