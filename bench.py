@@ -1,19 +1,22 @@
 #!/usr/bin/env python
 """Benchmark: FP64 recursive partition solve on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--n|--size N_PER_GPU]
-                    [--transport auto|p2p|nccl] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n|--size N_GLOBAL]
+                    [--c4] [--weak] [--transport auto|p2p|nccl] [--impl ours|reference]
 
 A step is one full solve (all levels, finishing solve, Stage 3) of an
-N = 1e8-unknown strictly dominant system per GPU with the kNN-predicted
-policy [64, 10, 32, 16] (config 3). Inputs are generated on the device with
-the generate_system distributions and stay resident in HBM (3.2 GB per GPU,
-25x the 126 MB L2, so no L2 flush is needed between steps). N > 1: one
-process per GPU (torchrun), contiguous row shards of the global system
-N_global = N x 1e8 (weak scaling); the one exchange per solve (8 doubles per
-rank) runs inside the finishing kernel over peer memory (transport "p2p",
-chosen by "auto" when every rank can open every peer's CUDA IPC mailbox;
-otherwise an NCCL all-gather); device time = max over ranks.
+N = 1e8-unknown strictly dominant system with the kNN-predicted policy
+[64, 10, 32, 16] (config 3, BASELINE.json's metric). Inputs are generated on
+the device with the generate_system distributions and stay resident in HBM
+(3.2 GB, 25x the 126 MB L2, so no L2 flush is needed between steps).
+N GPUs > 1: one process per GPU (torchrun), contiguous row shards of the SAME
+global system (strong scaling: N = 1e8 on 1/2/4/8 B200;
+--c4: N = 1e9, config 4; --weak: --n unknowns per GPU instead); each rank
+runs the single-GPU graph on its shard with the one exchange per solve
+(8 doubles per rank) inside the deepest level's cluster kernel over peer
+memory (transport "p2p", chosen by "auto" when every rank can open every
+peer's CUDA IPC mailbox; otherwise an NCCL all-gather); device time = max
+over ranks.
 
 `--impl reference` times the reference's own CPU solver (oracle/_ref: the
 unmodified reference headers, all host threads) on rank 0 only.
@@ -43,8 +46,11 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--n", "--size", dest="n", type=float, default=1e8,
-                   help="unknowns per GPU (--size under torchrun: its own --n* options shadow --n)")
+    p.add_argument("--n", "--size", dest="n", type=float, default=None,
+                   help="global unknowns (default 1e8; per GPU with --weak). Under torchrun use --size: "
+                        "its own --n* options shadow --n")
+    p.add_argument("--c4", action="store_true", help="config 4: N = 1e9 global")
+    p.add_argument("--weak", action="store_true", help="--n unknowns per GPU (weak scaling)")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=6)
@@ -56,7 +62,19 @@ def parse():
     p.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
                    help="multi-GPU exchange: fused peer-memory (p2p), NCCL all-gather, or p2p with "
                         "NCCL fallback (auto)")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.n is None:
+        a.n = 1e9 if a.c4 else 1e8
+    return a
+
+
+def _trace(msg):
+    if os.environ.get("TPB_BENCH_TRACE"):
+        print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
+
+def global_n(args, world):
+    return int(args.n) * world if args.weak else int(args.n)
 
 
 def hbm_peak():
@@ -177,7 +195,7 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    n_arm = int(args.n) * max(1, args.gpus)  # our arm's global N at this GPU count
+    n_arm = global_n(args, max(1, args.gpus))  # our arm's global N at this GPU count
     n = n_arm
     # bound the run: ~3 s per N=1e8 solve on 16 cores; keep the whole run ~<= 3 min
     budget_s = 150.0
@@ -211,7 +229,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "reference CPU solve_partition (oracle/_ref, reference headers)",
                    "n_per_step": n, "policy": [int(v) for v in sizes], "threads": cores},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
@@ -233,7 +251,13 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dist = None
     sharded_mode = world > 1 or args.force_sharded
+    stdout_fd = None
     if sharded_mode:
+        # NCCL (and the process-group bring-up) may print to fd 1: keep rank 0's
+        # stdout to the one JSON line by pointing fd 1 at stderr until then
+        sys.stdout.flush()
+        stdout_fd = os.dup(1)
+        os.dup2(2, 1)
         import torch.distributed as dist
         if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
             os.environ["NCCL_DEBUG"] = "WARN"  # keep rank 0's stdout to the one JSON line
@@ -244,10 +268,10 @@ def run_ours(args):
             dist.init_process_group("gloo")  # NCCL refuses two ranks on one GPU
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n_per = int(args.n)
-    n_glob = n_per * world
+    n_glob = global_n(args, world)
+    n_per = n_glob // world
     policy = tp.predicted_policy(n_glob)
-    lo, n_loc = sharded.shard_bounds(n_glob, world, rank)
+    lo, n_loc = sharded.shard_bounds(n_glob, world, rank, sharded.shard_granule(policy))
     stream = torch.cuda.current_stream()
     ctx = tp.context(local)
 
@@ -269,6 +293,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    _trace("setup done")
     # untimed: graph capture + clock ramp (~0.3 s of solves), then W warm-up steps
     step()
     barrier()
@@ -285,6 +310,7 @@ def run_ours(args):
         step()
     barrier()
 
+    _trace("warm-up done")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -303,6 +329,7 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = n_glob * args.steps / (ms / 1e3)
 
+    _trace("timed region done")
     # correctness of what was timed
     tp.check_device_error()
     res = tp.residual_inf(sys_d, x) if world == 1 else None
@@ -315,9 +342,12 @@ def run_ours(args):
         dist.all_reduce(num_d, op=dist.ReduceOp.MAX)
         res = float(num_d[0]) / max(1.0, float(num_d[1]))
 
-    # per-kernel durations (CUDA events on the launch stream, same inputs)
+    _trace("residual done")
+    # per-kernel durations (CUDA events on the launch stream, same inputs).
+    # Sharded: each rank times its shard's levels run standalone (the same
+    # kernels and shapes as its sharded graph, minus the peer exchange)
     prof = {}
-    if not sharded_mode:
+    if True:
         import ctypes as C
         from paper_2510_27351_b200._lib import TpError, lib
         sz = np.asarray(policy.sizes, dtype=np.int64)
@@ -338,7 +368,12 @@ def run_ours(args):
                 nm = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
                 prof.setdefault(nm, []).append(kms[i])
         prof = {k: statistics.median(v) for k, v in prof.items()}
+    per_rank = None
+    if dist is not None:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, {"rank": rank, "n_local": n_loc, "kernels_ms": prof})
 
+    _trace("profile done")
     # end to end through the public API: pinned host buffers, H2D + solve + D2H
     e2e = None
     h2d = 4 * 8 * n_loc
@@ -427,14 +462,16 @@ def run_ours(args):
         # inputs as the device-resident steps, so it must match them bit for bit
         e2e["result_matches_device_solve"] = bool(torch.equal(hx[(args.e2e_steps - 1) % 2], x.cpu()))
 
+    _trace("e2e done")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference(n_per, args.cpu_runs, args.seed)
+            cpu = cpu_reference(n_glob, args.cpu_runs, args.seed)
         except Exception as e:  # reference build missing on this box
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    _trace("cpu baseline done")
     if rank == 0:
         peak, peak_src = hbm_peak()
         roof = None
@@ -455,6 +492,9 @@ def run_ours(args):
                     traffic = None
             roof = {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic,
+                    "traffic_source": ("profiles/ncu_summary.json: committed `ncu --set full` capture of this "
+                                       "kernel on this workload (tools/ncu_capture.py), not measured by this run")
+                    if traffic is not None else None,
                     "peak_note": ("peak = the driver's copy bandwidth (1 read : 1 write); this kernel streams "
                                   "4 reads : 1 write, whose measured B200 ceiling with trivial compute is "
                                   f"{PATTERN_CEILING_GBS:.0f} GB/s (profiles/r01_microbench.md)"),
@@ -462,18 +502,33 @@ def run_ours(args):
                     "alg_bytes_per_launch": ALG_BYTES_PER_UNKNOWN * n_loc,
                     "kernel_ms": t_k, "peak_source": peak_src,
                     "kernel_share_of_step": t_k / sum(prof.values())}
+            if per_rank is not None:
+                roof["per_rank"] = []
+                for pr in per_rank:
+                    tk = pr["kernels_ms"].get(k)
+                    if tk:
+                        a_ = ALG_BYTES_PER_UNKNOWN * pr["n_local"] / (tk * 1e-3) / 1e9
+                        roof["per_rank"].append({"rank": pr["rank"], "n_local": pr["n_local"], "kernel_ms": tk,
+                                                 "achieved": a_, "frac": a_ / peak})
+                roof["note"] = ("per-rank kernel times from each rank's shard levels run standalone after the "
+                                "timed region (same kernels and shapes as the sharded graph)")
         solve_gbs = ALG_BYTES_PER_UNKNOWN * n_glob / (ms_step * 1e-3) / 1e9 / world
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic: device counter-based generator with generate_system's distributions",
-            "config": {"workload": "recursive partition solve, kNN policy, N=1e8 per GPU (config 3)",
+            "config": {"workload": (f"recursive partition solve, kNN policy, N={n_glob:.0e} "
+                                    + ("per GPU (weak)" if args.weak else "global")
+                                    + (" (config 4)" if n_glob == 10**9 else
+                                       " (config 3)" if n_glob == 10**8 else "")),
                        "n_per_gpu": n_per, "n_global": n_glob, "policy": policy.sizes,
-                       "l2": "inputs 3.2 GB/GPU >> 126 MB L2 (no flush)",
+                       "l2": f"inputs {32 * n_loc / 1e9:.2f} GB/GPU vs the 126 MB L2 (no flush)",
+                       "shard_granule_rows": sharded.shard_granule(policy) if sharded_mode else None,
                        "parallelism": "single GPU" if not sharded_mode else (
                            f"{world} contiguous shard(s) + " + (
-                               "fused peer-memory exchange in the finishing kernel (CUDA IPC)"
+                               "fused peer-memory exchange in the deepest level's cluster kernel (CUDA IPC)"
                                if solver.transport == "p2p" else "NCCL all-gather")),
                        "transport": None if not sharded_mode else solver.transport,
                        "transport_fallback": None if not sharded_mode else solver.fallback_reason},
@@ -490,6 +545,9 @@ def run_ours(args):
             "clocks": clk.summary(),
             "residual": res,
         }
+        if stdout_fd is not None:
+            sys.stdout.flush()
+            os.dup2(stdout_fd, 1)
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -69,6 +69,10 @@ tp_status tp_ctx_set_stream(tp_ctx* ctx, void* stream, tp_error* err);
 tp_status tp_ctx_set_graphs(tp_ctx* ctx, int32_t enabled, tp_error* err);
 /* Number of kernels the last solve on this context launched (0 if none). */
 int64_t tp_ctx_last_launch_count(const tp_ctx* ctx);
+/* Names ("kernel:Llevel", comma-separated) of the kernels of the last solve on
+ * this context, NUL-terminated into buf (cap bytes); returns the full length.
+ * Diagnostic: which fused / folded kernels a plan took. */
+int64_t tp_ctx_last_kernels(const tp_ctx* ctx, char* buf, int64_t cap);
 
 /* ---------------------------------------------------- the partition solve */
 /* solve_partition(sys, policy) — partition.hpp:244-248 (validation :235-242).

@@ -35,7 +35,7 @@ MALFORMED_HEADER, BAD_NUMBER, IO, CUDA, INVALID_ARGUMENT, NCCL = 6, 7, 8, 9, 10,
 
 EXPORTS = [
     "tp_abi_version", "tp_ctx_create", "tp_ctx_destroy", "tp_ctx_set_stream", "tp_ctx_set_graphs",
-    "tp_ctx_last_launch_count", "tp_solve_partition_f64", "tp_solve_partition_f64_dev",
+    "tp_ctx_last_launch_count", "tp_ctx_last_kernels", "tp_solve_partition_f64", "tp_solve_partition_f64_dev",
     "tp_check_device_error", "tp_solve_partition_observe_f64", "tp_thomas_solve_f64",
     "tp_residual_inf_f64_dev", "tp_shard_reduce_f64_dev", "tp_shard_finish_f64_dev",
     "tp_generate_system_f64_dev", "tp_make_plan", "tp_plan_levels", "tp_solve_profile_f64_dev",
@@ -65,6 +65,7 @@ def _load():
         "tp_ctx_set_stream": (C.c_int, [vp, vp, E]),
         "tp_ctx_set_graphs": (C.c_int, [vp, C.c_int32, E]),
         "tp_ctx_last_launch_count": (C.c_int64, [vp]),
+        "tp_ctx_last_kernels": (C.c_int64, [vp, C.c_char_p, C.c_int64]),
         "tp_solve_partition_f64": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp, E]),
         "tp_solve_partition_f64_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
                                                  vp, E]),

@@ -102,6 +102,7 @@ struct Plan {
     SysPtrs<T> final_in{};
     T* final_x = nullptr;
     size_t ws_elems = 0;  // workspace, in elements of T
+    int cs = 0;           // cluster shape of k_level_final_cl (0 = probed, 8 = portable)
 };
 
 inline size_t pad32(size_t v) { return (v + 31) & ~size_t(31); }
@@ -141,8 +142,9 @@ void push_chain(Plan<T>& p, Level<T> L, size_t& ws) {
 // added for it), and an oversized final system gets ONE fused internal level
 // of m = 16 when that fits. The sharded paths keep n_final <= kFinalCap.
 template <class T>
-void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p, bool fused = false) {
+void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p, bool fused = false, int cs = 0) {
     p.levels.clear();
+    p.cs = cs;
     int64_t cur = n;
     int lvl = 0;
     size_t ws = 0;
@@ -171,12 +173,12 @@ void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p, boo
     }
     // device-internal levels so the finishing solve fits one cluster
     const bool last_fused = fused && !p.levels.empty() && !p.levels.back().split &&
-                            tpb::level_final_fits(p.levels.back().n, p.levels.back().m, p.levels.back().K, sizeof(T));
+                            tpb::level_final_fits(p.levels.back().n, p.levels.back().m, p.levels.back().K, sizeof(T), cs);
     while (!last_fused && cur > tpb::kFinalCap) {
         Level<T> L;
         L.n = cur;
         L.m = kInternalM;
-        if (fused && tpb::level_final_fits(cur, kFusedInternalM, plan_blocks(cur, kFusedInternalM), sizeof(T)))
+        if (fused && tpb::level_final_fits(cur, kFusedInternalM, plan_blocks(cur, kFusedInternalM), sizeof(T), cs))
             L.m = kFusedInternalM;
         L.K = plan_blocks(cur, L.m);
         const int64_t last_len = cur - (L.K - 1) * L.m;
@@ -247,6 +249,7 @@ struct tp_ctx {
     unsigned long long* d_epoch = nullptr;
     tpb::ShardLink link{};
     bool linked = false;
+    bool link_shared = false;  // a peer's mailbox lives on this context's GPU
     int64_t link_gen = 0;
     std::vector<void*> ipc_opened;
     bool prepare_only = false;  // capture + instantiate the graph, do not launch
@@ -254,6 +257,7 @@ struct tp_ctx {
     void* dsys = nullptr;                 // host-path staging (5 arrays)
     size_t dsys_cap = 0;                  // bytes
     int64_t last_launches = 0;
+    std::string last_names;  // the last solve's kernels (Runner::names)
     // The last solve whose zero pivot tp_check_device_error / the synchronous
     // calls may have to locate in the reference's order (diagnose_pivot).
     struct LastSolve {
@@ -268,6 +272,7 @@ struct tp_ctx {
         std::vector<int64_t> key;
         cudaGraphExec_t exec = nullptr;
         int64_t launches = 0;
+        std::string names;
         uint64_t stamp = 0;
     };
     std::vector<GraphEntry> gcache;
@@ -288,13 +293,14 @@ struct Runner {
     int64_t launches = 0;
     cudaError_t status = cudaSuccess;
 
+    std::string names;  // "what:Llevel" of every kernel, comma-separated (tp_ctx_last_kernels)
     void after(const char* what, int level) {
         ++launches;
-        if (hook) {
-            char name[32];
-            std::snprintf(name, sizeof(name), "%s:L%d", what, level);
-            hook(hook_user, name);
-        }
+        char name[32];
+        std::snprintf(name, sizeof(name), "%s:L%d", what, level);
+        if (!names.empty()) names += ',';
+        names += name;
+        if (hook) hook(hook_user, name);
     }
     void check(cudaError_t e) {
         if (e != cudaSuccess && status == cudaSuccess) status = e;
@@ -373,16 +379,12 @@ struct Runner {
     // Whole solve: reset the error word, Stage 1 down, finish, Stage 3 up.
     void solve(const Plan<T>& p) {
         check(tpb::launch_reset(ctx->d_err, st));
+        ++launches;  // k_reset: counted, not timed by the profile hook
         solve_body(p);
     }
-    // The deepest level and the finishing solve run as one cluster kernel when
-    // that level fits the cluster's shared memory (k_level_final_cl); its
-    // interface is still written out (for the observer), never read back.
-    void solve_body(const Plan<T>& p) {
-        const size_t nl = p.levels.size();
-        const bool fuse = nl > 0 && !p.levels.back().split &&
-                          tpb::level_final_fits(p.levels.back().n, p.levels.back().m, p.levels.back().K, sizeof(T));
-        const size_t top = fuse ? nl - 1 : nl;
+    // Stage 1 of levels [0, top): level 1's (and level 2's) folded into level
+    // 0's kernel (k_fast_s1fold) where the shapes allow, the rest per level.
+    void stage1_down(const Plan<T>& p, size_t top) {
         size_t l = 0;
         if (top >= 2) {  // level 1's Stage 1 folded into level 0's (k_fast_s1fold)
             const Level<T>& A = p.levels[0];
@@ -400,10 +402,30 @@ struct Runner {
             }
         }
         for (; l < top; ++l) stage(p.levels[l], (int)l, tpb::kStage1);
+    }
+
+    // The deepest level and the finishing solve run as one cluster kernel when
+    // that level fits the cluster's shared memory (k_level_final_cl); its
+    // interface is still written out (for the observer), never read back.
+    // mode kShard (sharded plan, fused = true): the same graph with the peer
+    // exchange at the root of the deepest level (k_level_final_cl<kShard>) or
+    // of the finishing solve (k_final<kShard>).
+    void solve_body(const Plan<T>& p, int mode = tpb::kSolve) {
+        const size_t nl = p.levels.size();
+        const bool fuse = nl > 0 && !p.levels.back().split &&
+                          tpb::level_final_fits(p.levels.back().n, p.levels.back().m, p.levels.back().K, sizeof(T),
+                                                p.cs);
+        const size_t top = fuse ? nl - 1 : nl;
+        stage1_down(p, top);
         if (fuse) {
             const Level<T>& L = p.levels.back();
-            check(tpb::launch_level_final<T>(L.in, L.n, L.m, L.K, L.iface, L.x_out, ctx->d_err, (int)top, st));
-            after("level_final", (int)top);
+            check(tpb::launch_level_final<T>(L.in, L.n, L.m, L.K, L.iface, L.x_out, ctx->d_err, (int)top, st, mode,
+                                             mode == tpb::kShard ? &ctx->link : nullptr, p.cs));
+            after(mode == tpb::kShard ? "level_exchange" : "level_final", (int)top);
+        } else if (mode == tpb::kShard) {
+            check(tpb::launch_final<T>(tpb::kShard, p.final_in, p.n_final, IfacePtrs<T>{}, nullptr, p.final_x,
+                                       ctx->d_err, (int)p.levels.size(), st, &ctx->link));
+            after("shard_exchange", (int)p.levels.size());
         } else {
             final_solve(p);
         }
@@ -413,21 +435,20 @@ struct Runner {
     // Sharded halves.
     void shard_reduce(const Plan<T>& p, T* eq8) {
         check(tpb::launch_reset(ctx->d_err, st));
-        for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
+        ++launches;  // k_reset: counted, not timed by the profile hook
+        stage1_down(p, p.levels.size());
         IfacePtrs<T> o{eq8, eq8 + 2, eq8 + 4, eq8 + 6};
         check(tpb::launch_final<T>(tpb::kStage1, p.final_in, p.n_final, o, nullptr, nullptr, ctx->d_err,
                                    (int)p.levels.size(), st));
         after("shard_reduce", (int)p.levels.size());
     }
-    // Fused multi-GPU solve of one shard: every local level, the peer exchange
-    // and top solve inside the finishing kernel, every local Stage 3.
+    // Fused multi-GPU solve of one shard: the single-GPU graph (folded Stage 1,
+    // the deepest level fused with the finishing solve, Stage 3 up) with the
+    // peer exchange and the top solve at the root of the deepest level.
     void shard_solve(const Plan<T>& p) {
         check(tpb::launch_reset(ctx->d_err, st));
-        for (size_t l = 0; l < p.levels.size(); ++l) stage(p.levels[l], (int)l, tpb::kStage1);
-        check(tpb::launch_final<T>(tpb::kShard, p.final_in, p.n_final, IfacePtrs<T>{}, nullptr, p.final_x,
-                                   ctx->d_err, (int)p.levels.size(), st, &ctx->link));
-        after("shard_exchange", (int)p.levels.size());
-        for (size_t l = p.levels.size(); l-- > 0;) stage(p.levels[l], (int)l, tpb::kStage3);
+        ++launches;  // k_reset: counted, not timed by the profile hook
+        solve_body(p, tpb::kShard);
     }
     void shard_finish(const Plan<T>& p, const T* eq_all, int nranks, int rank) {
         T* x2 = static_cast<T*>(ctx->d_small);
@@ -536,6 +557,7 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
         Runner<T> r{ctx, st};
         fn(r);
         ctx->last_launches = r.launches;
+        ctx->last_names = r.names;
         if (r.status != cudaSuccess) {
             set_err(err, TP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(r.status));
             return TP_ERR_CUDA;
@@ -547,6 +569,7 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
             g.stamp = ++ctx->clock;
             if (!ctx->prepare_only) TP_CUDA(cudaGraphLaunch(g.exec, st));
             ctx->last_launches = g.launches;
+            ctx->last_names = g.names;
             return TP_OK;
         }
     }
@@ -594,9 +617,11 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
     ge.key = key;
     ge.exec = exec;
     ge.launches = r.launches;
+    ge.names = r.names;
     ge.stamp = ++ctx->clock;
     ctx->gcache.push_back(ge);
     ctx->last_launches = r.launches;
+    ctx->last_names = r.names;
     if (!ctx->prepare_only) TP_CUDA(cudaGraphLaunch(exec, st));
     if (dbg)
         std::fprintf(stderr, "[tpb graph] capture %.3f ms, instantiate %.3f ms, launch %.3f ms (%lld kernels)\n",
@@ -995,13 +1020,14 @@ tp_status shard_solve(tp_ctx* ctx, const T* sub, const T* diag, const T* super, 
     }
     TP_CUDA(cudaSetDevice(ctx->device));
     Plan<T> p;
-    build_plan(n_local, sizes, nsizes, p);
+    build_plan(n_local, sizes, nsizes, p, /*fused=*/true, ctx->link_shared ? 8 : 0);
     s = ensure_ws(ctx, p.ws_elems * sizeof(T), err);
     if (s != TP_OK) return s;
     bind_plan(p, SysPtrs<T>{sub, diag, super, rhs}, x_dev, ctx->ws);
     const cudaStream_t st = pick_stream(ctx, stream);
     ctx->last.kind = 0;
-    auto key = make_key<T>(5, n_local, sizes, nsizes, {sub, diag, super, rhs, x_dev, ctx->ws}, ctx->link_gen);
+    auto key = make_key<T>(5, n_local, sizes, nsizes, {sub, diag, super, rhs, x_dev, ctx->ws},
+                           ctx->link_gen * 2 + (ctx->link_shared ? 1 : 0));
     return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.shard_solve(p); }, err);
 }
 
@@ -1178,6 +1204,17 @@ tp_status tp_ctx_set_graphs(tp_ctx* ctx, int32_t enabled, tp_error* err) {
 }
 
 int64_t tp_ctx_last_launch_count(const tp_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+int64_t tp_ctx_last_kernels(const tp_ctx* ctx, char* buf, int64_t cap) {
+    if (!ctx) return 0;
+    const int64_t len = (int64_t)ctx->last_names.size();
+    if (buf && cap > 0) {
+        const int64_t k = len < cap - 1 ? len : cap - 1;
+        std::memcpy(buf, ctx->last_names.data(), (size_t)k);
+        buf[k] = '\0';
+    }
+    return len;
+}
 
 tp_status tp_check_device_error(tp_ctx* ctx, tp_error* err) {
     clear_err(err);
@@ -1389,6 +1426,20 @@ tp_status tp_shard_attach(tp_ctx* ctx, int32_t nranks, int32_t rank, void* const
     lk.nranks = nranks;
     lk.rank = rank;
     ctx->link = lk;
+    // peers on this very GPU (simulated ranks, TPB_SHARE_GPU): every rank's
+    // exchange kernel spins on one device, so they take the portable 8-CTA
+    // cluster shape (more of them co-resident, SMs left for the others' levels)
+    ctx->link_shared = false;
+    for (int p = 0; p < nranks; ++p) {
+        if (p == rank) continue;
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, mailboxes[p]) != cudaSuccess) {
+            cudaGetLastError();
+            ctx->link_shared = true;  // unknown: the conservative shape
+        } else if (pa.device == ctx->device) {
+            ctx->link_shared = true;
+        }
+    }
     ctx->linked = true;
     ++ctx->link_gen;  // graphs captured with the previous links stay keyed to them
     return TP_OK;

@@ -642,10 +642,14 @@ __device__ __forceinline__ void lf_expand_regs(T* a, const T* rbp, const T* gp, 
 // MF = m when m is 4, 8 or 16 (register sweeps for the full blocks), else 0.
 // CS = CTAs per cluster (8, or 16 where the GPU can co-schedule a
 // non-portable 16-CTA cluster); the cluster shape is set at launch.
-template <class T, int MF, int CS>
+// MODE kSolve: the interface root is solved here (single-GPU solve);
+// kShard: this level is a shard's deepest, its root pair is the shard's
+// boundary pair and goes through the peer exchange (shard_exchange) before the
+// tree unwinds — the multi-GPU graph then has the single-GPU graph's shape.
+template <class T, int MF, int CS, int MODE>
 __global__ void __launch_bounds__(kFinNT, 1)
     k_level_final_cl(SysPtrs<T> sys, int64_t n, int m, int64_t K, int S, IfacePtrs<T> iface, T* __restrict__ x,
-                     unsigned long long* err, int level) {
+                     unsigned long long* err, int level, const __grid_constant__ ShardLink link) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char lf_raw[];
@@ -715,10 +719,9 @@ __global__ void __launch_bounds__(kFinNT, 1)
     // ---- the interface (2K rows) across the cluster ----
     int per = 1;
     while (per * 2 <= kFinNT && per * 2 <= nb) per *= 2;
-    const ShardLink none{};
-    cl_tree<T, kSolve, CS>(cl, fa, fb, fc, fd, 2 * B0, 2 * nb, per,
-                       [&](int c) { return 2 * (K * c / CS); }, 2 * K, IfacePtrs<T>{}, nullptr, fx,
-                       2 * B0, bad_fin, err, level + 1, none);
+    cl_tree<T, MODE, CS>(cl, fa, fb, fc, fd, 2 * B0, 2 * nb, per,
+                         [&](int c) { return 2 * (K * c / CS); }, 2 * K, IfacePtrs<T>{}, nullptr, fx,
+                         2 * B0, bad_fin, err, level + 1, link);
     __syncthreads();
     TP_LF_TRACE(3);
 

@@ -393,44 +393,72 @@ static bool g_fuse_last = true;
 // co-schedule it, else 8; TPB_LF_CLUSTER=8 forces the portable shape
 static int g_lf_cs = 8;
 
-static size_t level_final_smem(int64_t m, int64_t K, size_t elem) {
-    return (size_t)4 * (size_t)((K + g_lf_cs - 1) / g_lf_cs) * (size_t)level_final_stride(m) * elem;
+static int lf_cluster(int cs) { return cs == 8 ? 8 : g_lf_cs; }
+static size_t level_final_smem(int64_t m, int64_t K, size_t elem, int c) {
+    return (size_t)4 * (size_t)((K + c - 1) / c) * (size_t)level_final_stride(m) * elem;
 }
 
-bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem) {
+bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem, int cs) {
     // m <= 16: above that the one-thread-per-block sweeps of the fused kernel
     // lose to the level kernels' lane trees (C2, m = 32: 24.7 vs 22.6 us per solve).
     // The interface may exceed kFinalCap: each CTA solves <= 2 * kLfMaxBlocks of it.
+    const int c = lf_cluster(cs);
     if (!g_fuse_last || !g_final_cluster || m < 4 || m > 16 || K < kFinClusterMin) return false;
-    if ((K + g_lf_cs - 1) / g_lf_cs > kLfMaxBlocks) return false;
+    if ((K + c - 1) / c > kLfMaxBlocks) return false;
     if ((K - 1) * m >= n || n - (K - 1) * m > m + 1) return false;  // make_plan's shape
-    return level_final_smem(m, K, elem) <= kLfDynSmem;
+    return level_final_smem(m, K, elem, c) <= kLfDynSmem;
 }
 
-template <class T, int CS>
-static void (*level_final_kernel(int64_t m))(SysPtrs<T>, int64_t, int, int64_t, int, IfacePtrs<T>, T*,
-                                              unsigned long long*, int) {
-    return m == 4 ? k_level_final_cl<T, 4, CS> : m == 8 ? k_level_final_cl<T, 8, CS>
-           : m == 16 ? k_level_final_cl<T, 16, CS> : k_level_final_cl<T, 0, CS>;
+template <class T>
+using LfKernel = void (*)(SysPtrs<T>, int64_t, int, int64_t, int, IfacePtrs<T>, T*, unsigned long long*, int,
+                          ShardLink);
+
+// kShard variants exist for FP64 only (the sharded C-ABI is FP64)
+template <class T, int CS, int MODE>
+static LfKernel<T> level_final_kernel(int64_t m) {
+    if constexpr (MODE == kShard && !std::is_same<T, double>::value) {
+        (void)m;
+        return nullptr;
+    } else {
+        return m == 4 ? k_level_final_cl<T, 4, CS, MODE> : m == 8 ? k_level_final_cl<T, 8, CS, MODE>
+               : m == 16 ? k_level_final_cl<T, 16, CS, MODE> : k_level_final_cl<T, 0, CS, MODE>;
+    }
 }
 
 template <class T>
 cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, const IfacePtrs<T>& iface,
-                               T* x, unsigned long long* err, int level, cudaStream_t st) {
-    if (!level_final_fits(n, m, K, sizeof(T))) return cudaErrorInvalidValue;
-    auto k = g_lf_cs == 16 ? level_final_kernel<T, 16>(m) : level_final_kernel<T, 8>(m);
-    return launch_kc(level, (unsigned)g_lf_cs, k, (unsigned)g_lf_cs, kFinNT, level_final_smem(m, K, sizeof(T)), st,
-                     sys, n, (int)m, K, level_final_stride(m), iface, x, err, level);
+                               T* x, unsigned long long* err, int level, cudaStream_t st, int mode,
+                               const ShardLink* link, int cs) {
+    if (!level_final_fits(n, m, K, sizeof(T), cs)) return cudaErrorInvalidValue;
+    const int c = lf_cluster(cs);
+    LfKernel<T> k = nullptr;
+    if (mode == kShard) {
+        if (link == nullptr || link->nranks < 1 || link->nranks > kMaxPeers) return cudaErrorInvalidValue;
+        k = c == 16 ? level_final_kernel<T, 16, kShard>(m) : level_final_kernel<T, 8, kShard>(m);
+    } else {
+        k = c == 16 ? level_final_kernel<T, 16, kSolve>(m) : level_final_kernel<T, 8, kSolve>(m);
+    }
+    if (k == nullptr) return cudaErrorInvalidValue;
+    const ShardLink none{};
+    return launch_kc(level, (unsigned)c, k, (unsigned)c, kFinNT, level_final_smem(m, K, sizeof(T), c), st, sys, n,
+                     (int)m, K, level_final_stride(m), iface, x, err, level, link != nullptr ? *link : none);
 }
 
-template <class T, int CS>
-static cudaError_t set_level_final_attributes() {
+template <class T, int CS, int MODE>
+static cudaError_t set_level_final_attributes_m() {
     cudaError_t e = cudaSuccess;
     for (int64_t m : {4, 8, 16, 0}) {
-        auto k = level_final_kernel<T, CS>(m);
+        auto k = level_final_kernel<T, CS, MODE>(m);
+        if (k == nullptr) continue;
         if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLfDynSmem);
         if (e == cudaSuccess && CS > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     }
+    return e;
+}
+template <class T, int CS>
+static cudaError_t set_level_final_attributes() {
+    cudaError_t e = set_level_final_attributes_m<T, CS, kSolve>();
+    if (e == cudaSuccess) e = set_level_final_attributes_m<T, CS, kShard>();
     return e;
 }
 
@@ -453,7 +481,7 @@ static int probe_level_final_cluster() {
     cfg.attrs = &at;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)k_level_final_cl<double, 16, 16>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)k_level_final_cl<double, 16, 16, kSolve>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 8;
     }
@@ -568,8 +596,8 @@ cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsign
                                         int64_t, int64_t, const IfacePtrs<T>&, const IfacePtrs<T>*,        \
                                         unsigned long long*, int, cudaStream_t);                        \
     template cudaError_t launch_level_final<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t,        \
-                                               const IfacePtrs<T>&, T*,                             \
-                                               unsigned long long*, int, cudaStream_t);             \
+                                               const IfacePtrs<T>&, T*, unsigned long long*, int,   \
+                                               cudaStream_t, int, const ShardLink*, int);           \
     template cudaError_t launch_split<T>(int, const SysPtrs<T>&, int64_t, int64_t, int64_t, int64_t,   \
                                          int64_t, const IfacePtrs<T>&, const T*, T*,                \
                                          unsigned long long*, int, cudaStream_t);                   \

@@ -99,10 +99,14 @@ cudaError_t launch_fold(int64_t m0, bool vec, const SysPtrs<T>& sys, int64_t K0,
 // level_final_fits says whether a level of n rows in K blocks of m fits the
 // cluster's shared memory; launch_level_final returns cudaErrorInvalidValue
 // when it does not (the caller then runs the three-kernel form).
-bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem);
+// mode kSolve (single system) or kShard (FP64: the shard's root pair goes
+// through the peer exchange of `link`); cs = 8 forces the portable 8-CTA
+// cluster (ranks sharing one GPU), 0 = the probed shape (16 where it fits).
+bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem, int cs = 0);
 template <class T>
 cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, const IfacePtrs<T>& iface,
-                               T* x, unsigned long long* err, int level, cudaStream_t st);
+                               T* x, unsigned long long* err, int level, cudaStream_t st, int mode = kSolve,
+                               const ShardLink* link = nullptr, int cs = 0);
 // One split level (tp_split.cuh): nblocks blocks of blen rows starting at
 // row_base, nsub chunks each, chunk pairs written from pair q_base on.
 template <class T>

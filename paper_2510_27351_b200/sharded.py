@@ -33,14 +33,37 @@ from .tridpart import (RecursionPolicy, _call, _policy_array, _raise, context, p
                        torch_stream)
 
 
-def shard_bounds(n_global: int, nranks: int, rank: int):
-    """Contiguous, near-equal shards; every shard keeps >= 2 rows."""
+def shard_granule(policy) -> int:
+    """Row granule that keeps a shard's first two levels free of tail blocks:
+    m0 * m1 / 2 when m1 is even (level-1 blocks are whole groups of m1/2
+    level-0 blocks — the shape the folded Stage-1 kernel needs, so every rank
+    runs the single-GPU graph), else m0. C3 [64,10,...]: 320 rows."""
+    sizes = list(policy.sizes if hasattr(policy, "sizes") else policy)
+    if not sizes:
+        return 1
+    g = int(sizes[0])
+    if len(sizes) > 1 and int(sizes[1]) % 2 == 0:
+        g *= int(sizes[1]) // 2
+    return max(1, g)
+
+
+def shard_bounds(n_global: int, nranks: int, rank: int, granule: int = 1):
+    """Contiguous, near-equal shards whose boundaries fall on multiples of
+    `granule` rows (the last shard takes the remainder); every shard keeps
+    >= 2 rows. Falls back to granule 1 when the system is too small for it.
+    The partition is the caller's choice: any contiguous split solves the same
+    global system; aligned splits keep each shard's plan free of
+    level-0/1 tails."""
     if nranks < 1 or not 0 <= rank < nranks:
         raise ValueError("bad rank / world size")
     if n_global < 2 * nranks:
         raise ValueError("every shard needs at least 2 rows")
-    lo = rank * n_global // nranks
-    hi = (rank + 1) * n_global // nranks
+    g = max(1, int(granule))
+    units = n_global // g
+    if units < nranks or g * (units // nranks) < 2:
+        g, units = 1, n_global
+    lo = (rank * units // nranks) * g
+    hi = n_global if rank == nranks - 1 else ((rank + 1) * units // nranks) * g
     return lo, hi - lo
 
 
@@ -208,15 +231,23 @@ class ShardedSolver:
         torch.cuda.synchronize()
         err = TpError()
         st = lib.tp_check_device_error(self.backend.ctx.handle, C.byref(err))
+        me = dist.get_rank(self.group)
         mine = None
         if st == NCCL:
-            mine = f"rank {dist.get_rank(self.group)}: {err.msg.decode(errors='replace')}"
+            mine = ("exchange", f"rank {me}: {err.msg.decode(errors='replace')}")
         elif st != 0:
-            _raise(st, err)  # a genuine solver error (zero pivot, ...)
+            # a genuine solver error (zero pivot, ...): still join the gather
+            # below, so a rank-local error cannot leave the peers blocked in it
+            mine = ("solver", me)
         verdicts = [None] * dist.get_world_size(self.group)
         dist.all_gather_object(verdicts, mine, group=self.group)
         self._verified = True
-        failed = [v for v in verdicts if v is not None]
+        if st != 0 and st != NCCL:
+            _raise(st, err)
+        solver_ranks = [v[1] for v in verdicts if v is not None and v[0] == "solver"]
+        if solver_ranks:
+            raise RuntimeError(f"solver error on rank(s) {solver_ranks} (raised there)")
+        failed = [v[1] for v in verdicts if v is not None]
         if not failed:
             return x
         self.transport = "nccl"
@@ -259,7 +290,7 @@ def simulate_ranks(sub, diag, sup, rhs, nranks: int, policy=None) -> np.ndarray:
     arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (sub, diag, sup, rhs)]
     shards, ctxs, eqs = [], [], []
     for r in range(nranks):
-        lo, cnt = shard_bounds(n, nranks, r)
+        lo, cnt = shard_bounds(n, nranks, r, shard_granule(pol))
         sys4 = [torch.from_numpy(a[lo:lo + cnt].copy()).cuda() for a in arrs]
         be = DeviceBackend(Context(torch.cuda.current_device()))
         eqs.append(be.reduce(sys4, pol))
@@ -277,7 +308,7 @@ def simulate_ranks(sub, diag, sup, rhs, nranks: int, policy=None) -> np.ndarray:
     return x
 
 
-def simulate_ranks_fused(sub, diag, sup, rhs, nranks: int, policy=None, repeats: int = 1):
+def simulate_ranks_fused(sub, diag, sup, rhs, nranks: int, policy=None, repeats: int = 1, kernels=None):
     """The fused peer-memory path with `nranks` simulated ranks on ONE GPU:
     one context (own stream) per rank, mailboxes linked by raw pointers, all
     ranks' graphs in flight at once (their finishing kernels wait on each
@@ -298,7 +329,7 @@ def simulate_ranks_fused(sub, diag, sup, rhs, nranks: int, policy=None, repeats:
     attach_local_peers(ctxs)
     shards = []
     for r in range(nranks):
-        lo, cnt = shard_bounds(n, nranks, r)
+        lo, cnt = shard_bounds(n, nranks, r, shard_granule(pol))
         sys4 = [torch.from_numpy(a[lo:lo + cnt].copy()).cuda() for a in arrs]
         # size each context's workspace up front (same plan as the fused solve)
         # so no allocation happens while other ranks' kernels wait on flags
@@ -319,6 +350,8 @@ def simulate_ranks_fused(sub, diag, sup, rhs, nranks: int, policy=None, repeats:
             _raise(lib.tp_check_device_error(ctxs[r].handle, C.byref(err)), err)
             x[lo:lo + cnt] = xr.cpu().numpy()
         xs.append(x)
+    if kernels is not None:  # each rank's kernel list (tp_ctx_last_kernels)
+        kernels.extend(c.last_kernels() for c in ctxs)
     for c in ctxs:
         c.close()
     return xs[0] if repeats == 1 else xs

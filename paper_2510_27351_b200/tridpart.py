@@ -149,6 +149,13 @@ class Context:
     def last_launch_count(self) -> int:
         return int(lib.tp_ctx_last_launch_count(self.handle))
 
+    def last_kernels(self) -> list:
+        """The last solve's kernels, "name:Llevel" in launch order (k_reset not listed)."""
+        n = int(lib.tp_ctx_last_kernels(self.handle, None, 0))
+        buf = C.create_string_buffer(n + 1)
+        lib.tp_ctx_last_kernels(self.handle, buf, n + 1)
+        return [k for k in buf.value.decode().split(",") if k]
+
 
 _tls = threading.local()
 

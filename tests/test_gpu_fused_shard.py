@@ -90,6 +90,37 @@ print(json.dumps({"m": out, "same": bool(np.array_equal(xs[0], xs[1]) and np.arr
 
 
 @needs_shared_gpu
+@pytest.mark.parametrize("n,P", [(40_000_000, 8), (12_800_000, 2), (8_000_000, 1)])
+def test_fused_shard_runs_the_single_gpu_graph(tp, n, P):
+    """Each rank of the fused multi-GPU solve runs the single-GPU graph on its
+    shard: granule-aligned shards (m0*m1/2 rows) keep levels 0-1 tail-free, so
+    Stage 1 of levels 0-2 is the folded kernel and the deepest level is the
+    fused cluster kernel with the peer exchange at its root — the same kernels,
+    in the same order, as a single-GPU solve of a shard-sized system."""
+    m = _run_sim(_METRICS + f"""
+n, P = {n}, {P}
+pol = [64, 10, 32, 16]
+s = oracle.generate_system(n, 31)
+ref = oracle.solve_partition(s, pol)
+ks = []
+x = sharded.simulate_ranks_fused(s.sub, s.diag, s.sup, s.rhs, P, pol, kernels=ks)
+g = sharded.shard_granule(pol)
+single = []
+for r in range(P):
+    lo, cnt = sharded.shard_bounds(n, P, r, g)
+    sysr = tp.TridiagonalSystem(*(a[lo:lo + cnt].copy() for a in (s.sub, s.diag, s.sup, s.rhs)))
+    tp.solve_partition(sysr, tp.RecursionPolicy(pol))
+    single.append(tp.context().last_kernels())
+print(json.dumps({{"m": metrics(s, x, ref), "ks": ks, "single": single}}))
+""")
+    assert _ok(m["m"]), m["m"]
+    for ks, single in zip(m["ks"], m["single"]):
+        assert ks[0] == "stage1_fold2:L0", ks
+        assert "level_exchange:L3" in ks, ks
+        assert [k.replace("level_exchange", "level_final") for k in ks] == single, (ks, single)
+
+
+@needs_shared_gpu
 def test_fused_matches_nccl_path_algebra(tp):
     """Fused and host-gathered paths compute the same top system: results
     agree to rounding."""
@@ -207,8 +238,8 @@ def test_fused_two_processes_cuda_ipc(tp, oracle_mod):
 
 
 @needs_shared_gpu
-@pytest.mark.parametrize("world,transport", [(2, "auto"), (3, "nccl")])
-def test_bench_multi_rank_flow_on_one_gpu(world, transport):
+@pytest.mark.parametrize("world,transport,weak", [(2, "auto", False), (3, "nccl", True), (4, "auto", False)])
+def test_bench_multi_rank_flow_on_one_gpu(world, transport, weak):
     """bench.py's N>1 path (torchrun, one process per rank, sharded solve,
     max-over-ranks timing, one JSON line from rank 0) with every rank on the
     one GPU of this box (TPB_SHARE_GPU=1: gloo process group, the ranks
@@ -221,15 +252,18 @@ def test_bench_multi_rank_flow_on_one_gpu(world, transport):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", str(world), "--steps", "3", "--warmup", "3", "--prewarm", "0", "--e2e-steps", "1",
-           "--size", "4e6", "--transport", transport]
+           "--size", "4e6", "--transport", transport] + (["--weak"] if weak else [])
     out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == world and d["config"]["n_global"] == 4_000_000 * world
+    # strong scaling by default (the BASELINE metric: the same N on 1/2/4/8 GPUs)
+    assert d["n_gpus"] == world and d["config"]["n_global"] == 4_000_000 * (world if weak else 1)
+    assert d["scaling"] == ("weak" if weak else "strong")
     assert d["config"]["transport"] == ("p2p" if transport == "auto" else "nccl")
     assert d["residual"] <= 1e-12 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert len(d["roofline"]["per_rank"]) == world
 
 
 @needs_shared_gpu

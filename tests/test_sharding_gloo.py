@@ -124,6 +124,31 @@ def test_shard_bounds():
         shard_bounds(3, 2, 0)
 
 
+def test_shard_bounds_granule():
+    """Aligned shards: every boundary on a multiple of the granule (m0*m1/2,
+    so each shard's level 0 and level 1 have no tail block and the rank runs
+    the folded single-GPU graph); the last shard takes the remainder."""
+    from paper_2510_27351_b200.sharded import shard_bounds, shard_granule
+
+    assert shard_granule([64, 10, 32, 16]) == 320
+    assert shard_granule([64, 10, 32, 32]) == 320
+    assert shard_granule([32]) == 32
+    assert shard_granule([16, 5]) == 16
+    for n, P, g in ((10**8, 8, 320), (10**8, 2, 320), (10**9, 8, 320), (100_003, 3, 32), (1000, 4, 320),
+                    (7, 3, 320)):
+        spans = [shard_bounds(n, P, r, g) for r in range(P)]
+        assert spans[0][0] == 0 and sum(c for _, c in spans) == n
+        for (lo, c), (lo2, _) in zip(spans, spans[1:]):
+            assert lo + c == lo2
+        assert all(c >= 2 for _, c in spans)
+        if n // g >= P:
+            assert all(lo % g == 0 for lo, _ in spans)
+            assert all(c % g == 0 for _, c in spans[:-1])
+            assert max(c for _, c in spans) - min(c for _, c in spans) <= g + n % g
+    # N = 1e8 on 8 ranks: 39,062 or 39,063 granules of 320 rows each
+    assert {c for _, c in (shard_bounds(10**8, 8, r, 320) for r in range(8))} == {12_499_840, 12_500_160}
+
+
 def test_assemble_top_system_layout():
     from paper_2510_27351_b200.sharded import assemble_top_system
 
