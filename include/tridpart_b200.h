@@ -260,6 +260,11 @@ tp_status tp_solve_profile_f64_dev(tp_ctx* ctx, const double* sub, const double*
  * one cubic Newton step) and the correctly rounded 1/x over n random x. */
 int tp_diag_rcp_ulp(int64_t n, uint64_t seed, uint64_t* max_ulp);
 
+/* Diagnostic: %globaltimer phase stamps (8 per CTA: start, staged, leaves,
+ * pair published, barrier passed, top tree done, expanded, stored) of the last
+ * k_grid_solve launched with TPB_GRID_TRACE=1. Returns a cudaError_t. */
+int tp_debug_grid_trace(unsigned long long* out, int count);
+
 /* ------------------------------------------------------ kNN predictors */
 /* predict(model, n) — knn.hpp:57-77 (feature_of :38): k-NN on log10(N);
  * distance ties -> smaller N, vote ties -> smaller label. Host code. */

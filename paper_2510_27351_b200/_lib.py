@@ -40,7 +40,7 @@ EXPORTS = [
     "tp_residual_inf_f64_dev", "tp_shard_reduce_f64_dev", "tp_shard_finish_f64_dev",
     "tp_generate_system_f64_dev", "tp_make_plan", "tp_plan_levels", "tp_solve_profile_f64_dev",
     "tp_predict", "tp_fit_knn", "tp_recursion_sizes", "tp_default_model", "tp_obs_read",
-    "tp_obs_get", "tp_obs_free", "tp_diag_rcp_ulp", "tp_solve_partition_f32",
+    "tp_obs_get", "tp_obs_free", "tp_diag_rcp_ulp", "tp_debug_grid_trace", "tp_solve_partition_f32",
     "tp_solve_partition_f32_dev", "tp_solve_partition_observe_f32", "tp_thomas_solve_f32",
     "tp_residual_inf_f32_dev", "tp_generate_system_f32_dev", "tp_solve_partition_f64_async",
     "tp_solve_partition_f32_async", "tp_shard_mailbox", "tp_ipc_get_handle", "tp_ipc_open_handle",
@@ -93,6 +93,7 @@ def _load():
         "tp_obs_get": (C.c_int, [vp, C.c_int64, C.POINTER(TpObservation), _I32, _D, E]),
         "tp_obs_free": (None, [vp]),
         "tp_diag_rcp_ulp": (C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_uint64)]),
+        "tp_debug_grid_trace": (C.c_int, [C.c_void_p, C.c_int]),
         "tp_solve_partition_f32": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp, E]),
         "tp_solve_partition_f32_dev": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp,
                                                  vp, E]),

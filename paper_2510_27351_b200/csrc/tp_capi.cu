@@ -98,6 +98,8 @@ struct Level {
 template <class T>
 struct Plan {
     std::vector<Level<T>> levels;
+    int64_t n0 = 0, m0 = 0;  // the system and the policy's level-0 block size
+    int32_t npol = 0;        // policy levels
     int64_t n_final = 0;
     SysPtrs<T> final_in{};
     T* final_x = nullptr;
@@ -145,6 +147,9 @@ template <class T>
 void build_plan(int64_t n, const int64_t* sizes, int32_t nsizes, Plan<T>& p, bool fused = false, int cs = 0) {
     p.levels.clear();
     p.cs = cs;
+    p.n0 = n;
+    p.m0 = nsizes > 0 ? sizes[0] : 0;
+    p.npol = nsizes;
     int64_t cur = n;
     int lvl = 0;
     size_t ws = 0;
@@ -243,6 +248,8 @@ struct tp_ctx {
     unsigned long long* h_err = nullptr;
     unsigned long long* d_red = nullptr;  // residual / scratch words
     void* d_small = nullptr;              // shard scratch (x2 + gather scratch)
+    void* d_grid = nullptr;               // k_grid_solve: barrier word + CTA pairs
+    bool no_grid = false;                 // observer solves: keep the level path (interfaces in HBM)
     // fused multi-GPU path (k_final<kShard>): own mailbox, peer links, epoch word
     void* mailbox = nullptr;
     int mailbox_ranks = 0;
@@ -283,6 +290,20 @@ namespace {
 
 
 using KernelHook = void (*)(void* user, const char* name);
+
+// k_grid_solve takes the whole solve of a one-level policy whose rows fit the
+// grid's shared memory (TPB_GRID=0 disables it; TPB_GRID_MIN sets the
+// smallest n it takes, default kGridDefaultMin).
+constexpr int64_t kGridDefaultMin = 4;
+template <class T>
+bool use_grid(const tp_ctx* ctx, const Plan<T>& p) {
+    static const int64_t gmin = [] {
+        const char* v = getenv("TPB_GRID_MIN");
+        return v ? (int64_t)atoll(v) : kGridDefaultMin;
+    }();
+    if (ctx->no_grid || p.npol != 1 || p.levels.empty() || p.n0 < gmin || p.n0 < 4) return false;
+    return tpb::grid_fits(p.n0, p.m0, sizeof(T), ctx->sms);
+}
 
 template <class T>
 struct Runner {
@@ -376,11 +397,14 @@ struct Runner {
         after("final", (int)p.levels.size());
     }
 
-    // Whole solve: reset the error word, Stage 1 down, finish, Stage 3 up.
+    // Whole solve: reset the error word, Stage 1 down, finish, Stage 3 up —
+    // or, for a one-level policy that fits the grid's shared memory, the one
+    // co-resident kernel k_grid_solve (tp_grid.cu).
     void solve(const Plan<T>& p) {
-        check(tpb::launch_reset(ctx->d_err, st));
+        const bool grid = use_grid(ctx, p);
+        check(tpb::launch_reset(ctx->d_err, st, grid ? static_cast<unsigned*>(ctx->d_grid) : nullptr));
         ++launches;  // k_reset: counted, not timed by the profile hook
-        solve_body(p);
+        solve_body(p, tpb::kSolve, grid);
     }
     // Stage 1 of levels [0, top): level 1's (and level 2's) folded into level
     // 0's kernel (k_fast_s1fold) where the shapes allow, the rest per level.
@@ -410,7 +434,14 @@ struct Runner {
     // mode kShard (sharded plan, fused = true): the same graph with the peer
     // exchange at the root of the deepest level (k_level_final_cl<kShard>) or
     // of the finishing solve (k_final<kShard>).
-    void solve_body(const Plan<T>& p, int mode = tpb::kSolve) {
+    void solve_body(const Plan<T>& p, int mode = tpb::kSolve, bool bar_zeroed = false) {
+        if (mode == tpb::kSolve && use_grid(ctx, p)) {
+            const Level<T>& L0 = p.levels[0];
+            if (!bar_zeroed) check(cudaMemsetAsync(ctx->d_grid, 0, sizeof(unsigned), st));
+            check(tpb::launch_grid_solve<T>(L0.in, p.n0, p.m0, L0.x_out, ctx->d_grid, ctx->d_err, 0, ctx->sms, st));
+            after("grid_solve", 0);
+            return;
+        }
         const size_t nl = p.levels.size();
         const bool fuse = nl > 0 && !p.levels.back().split &&
                           tpb::level_final_fits(p.levels.back().n, p.levels.back().m, p.levels.back().K, sizeof(T),
@@ -535,6 +566,10 @@ tp_status decode_device_error(tp_ctx* ctx, tp_error* err) {
     if (code == tpb::kNoError) return TP_OK;
     const int32_t level = (int32_t)(code >> 48);
     const int64_t row = (int64_t)(code & 0xFFFFFFFFFFFFULL);
+    if (level == tpb::kGridBarrierLevel) {
+        set_err(err, TP_ERR_CUDA, "grid solve: CTA " + std::to_string(row) + " timed out at the grid barrier", row, -1);
+        return TP_ERR_CUDA;
+    }
     if (level == tpb::kExchangeLevel) {
         set_err(err, TP_ERR_NCCL, "peer exchange timed out waiting for rank " + std::to_string(row), row, -1);
         return TP_ERR_NCCL;
@@ -670,7 +705,7 @@ tp_status solve_dev(tp_ctx* ctx, const T* sub, const T* diag, const T* super, co
     ctx->last.in[2] = super;
     ctx->last.in[3] = rhs;
     ctx->last.x = x;
-    auto key = make_key<T>(1, n, sizes, nsizes, {sub, diag, super, rhs, x, ctx->ws});
+    auto key = make_key<T>(1, n, sizes, nsizes, {sub, diag, super, rhs, x, ctx->ws}, ctx->no_grid ? 1 : 0);
     return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.solve(p); }, err);
 }
 
@@ -696,6 +731,14 @@ tp_status diagnose_pivot(tp_ctx* ctx, int64_t dev_row, int32_t dev_level, tp_err
     bind_plan(p, SysPtrs<T>{(const T*)ls.in[0], (const T*)ls.in[1], (const T*)ls.in[2], (const T*)ls.in[3]},
               (T*)ls.x, ctx->ws);
     const cudaStream_t st = ctx->own;
+    if (use_grid(ctx, p)) {
+        // k_grid_solve keeps level 0's interface on chip: assemble it now
+        // (the same Stage-1 kernels and arithmetic as the level path)
+        Runner<T> r{ctx, st};
+        r.stage1_down(p, p.levels.size());
+        TP_CUDA(r.status);
+        TP_CUDA(cudaStreamSynchronize(st));
+    }
     int64_t kmax = 1;
     for (const auto& L : p.levels) kmax = std::max(kmax, L.K);
     void* scratch = nullptr;
@@ -848,7 +891,10 @@ tp_status solve_observe(tp_ctx* ctx, const T* sub, const T* diag, const T* super
                         int64_t n, const int64_t* sizes, int32_t nsizes, T* x,
                         void (*emit)(int64_t, int64_t, const T*, const T*, const T*, const T*, void*),
                         void* user, tp_error* err) {
+    // the observer reads every level's interface back: keep the level path
+    ctx->no_grid = emit != nullptr;
     tp_status s = solve_host<T>(ctx, sub, diag, super, rhs, n, sizes, nsizes, x, err);
+    ctx->no_grid = false;
     if (emit == nullptr || (s != TP_OK && s != TP_ERR_ZERO_PIVOT)) return s;
     // the reference calls the observer after each level's assembly
     // (partition.hpp:205-206): a zero pivot in level l's Stage 1 (or in the
@@ -1158,6 +1204,8 @@ tp_status tp_ctx_create(int32_t device, tp_ctx** out, tp_error* err) {
     if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 64);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_red, 64);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_small, 4096);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_grid, tpb::kGridScratchBytes);
+    if (e == cudaSuccess) e = cudaMemset(c->d_grid, 0, tpb::kGridScratchBytes);
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_err, 64);
     if (e != cudaSuccess) {
         set_err(err, TP_ERR_CUDA, std::string("context allocation: ") + cudaGetErrorString(e));
@@ -1178,6 +1226,7 @@ void tp_ctx_destroy(tp_ctx* ctx) {
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->d_red) cudaFree(ctx->d_red);
     if (ctx->d_small) cudaFree(ctx->d_small);
+    if (ctx->d_grid) cudaFree(ctx->d_grid);
     for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     if (ctx->mailbox) cudaFree(ctx->mailbox);
     if (ctx->d_epoch) cudaFree(ctx->d_epoch);

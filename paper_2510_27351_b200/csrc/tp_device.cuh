@@ -304,6 +304,70 @@ __device__ __forceinline__ T first_from_e1(const Eq2<T>& B, T xt, T xe) {
     return (B.d1 - B.a1 * xt - B.g1 * xe) * rcp(B.b1);
 }
 
+// ---------------------------------------------------------------------------
+// The same merge as ONE 2x2 elimination (Schur complement of the middle
+// block): A.E2 and B.E1 couple the middle unknowns (x_t, x_{t+1}) through
+//   [A.b2 A.g2; B.a1 B.b1] [x_t; x_{t+1}] = [A.d2 - A.a2 x_s; B.d1 - B.g1 x_e],
+// det = A.b2 B.b1 - A.g2 B.a1 = B.b1 * beta1 = A.b2 * bp (the pivots of the
+// up- and down-sweep of `merge`). One reciprocal instead of four: the merged
+// rows are ready after det -> rcp -> one FMA (~90 dependent cycles against
+// ~150 for `merge`), and the top-down step needs no reciprocal at all:
+//   x_t     = sd - sa x_s + sg x_e,    x_{t+1} = ud + ua x_s - ug x_e.
+// The pivot check sees the same four pivots as `merge` (B.b1, A.b2 directly,
+// beta1 and bp through det), off the critical path; `flag` records a failure.
+// ---------------------------------------------------------------------------
+template <class T>
+struct SchurSave {
+    T sd, sa, sg, ud, ua, ug;
+};
+
+template <class T>
+__device__ __forceinline__ Eq2<T> merge_schur(const Eq2<T>& A, const Eq2<T>& B, bool& flag, SchurSave<T>& sv) {
+    const T det = fma(A.b2, B.b1, -(A.g2 * B.a1));
+    const T r = rcp(det);
+    const T fl = pivot_floor<T>();
+    flag |= (fabs(B.b1) < fl) | (fabs(A.b2) < fl) | (fabs(det) < fl * fabs(B.b1)) | (fabs(det) < fl * fabs(A.b2));
+    sv.sd = fma(B.b1, A.d2, -(A.g2 * B.d1)) * r;
+    sv.sa = (B.b1 * A.a2) * r;
+    sv.sg = (A.g2 * B.g1) * r;
+    sv.ud = fma(A.b2, B.d1, -(B.a1 * A.d2)) * r;
+    sv.ua = (B.a1 * A.a2) * r;
+    sv.ug = (A.b2 * B.g1) * r;
+    Eq2<T> P;
+    P.a1 = A.a1;
+    P.b1 = fma(-A.g1, sv.sa, A.b1);
+    P.g1 = A.g1 * sv.sg;
+    P.d1 = fma(-A.g1, sv.sd, A.d1);
+    P.a2 = B.a2 * sv.ua;
+    P.b2 = fma(-B.a2, sv.ug, B.b2);
+    P.g2 = B.g2;
+    P.d2 = fma(-B.a2, sv.ud, B.d2);
+    return P;
+}
+// Stage-1-only form (no saves): every output row is one FMA after rcp(det).
+template <class T>
+__device__ __forceinline__ Eq2<T> merge_schur_up(const Eq2<T>& A, const Eq2<T>& B, bool& flag) {
+    const T det = fma(A.b2, B.b1, -(A.g2 * B.a1));
+    const T r = rcp(det);
+    const T fl = pivot_floor<T>();
+    flag |= (fabs(B.b1) < fl) | (fabs(A.b2) < fl) | (fabs(det) < fl * fabs(B.b1)) | (fabs(det) < fl * fabs(A.b2));
+    Eq2<T> P;
+    P.a1 = A.a1;
+    P.b1 = fma(-(A.g1 * B.b1 * A.a2), r, A.b1);
+    P.g1 = (A.g1 * A.g2 * B.g1) * r;
+    P.d1 = fma(-A.g1 * fma(B.b1, A.d2, -(A.g2 * B.d1)), r, A.d1);
+    P.a2 = (B.a2 * B.a1 * A.a2) * r;
+    P.b2 = fma(-(B.a2 * A.b2 * B.g1), r, B.b2);
+    P.g2 = B.g2;
+    P.d2 = fma(-B.a2 * fma(A.b2, B.d1, -(B.a1 * A.d2)), r, B.d2);
+    return P;
+}
+template <class T>
+__device__ __forceinline__ void schur_down(const SchurSave<T>& sv, T xs, T xe, T& xt, T& xt1) {
+    xt = fma(sv.sg, xe, fma(-sv.sa, xs, sv.sd));
+    xt1 = fma(-sv.ug, xe, fma(sv.ua, xs, sv.ud));
+}
+
 // Solve the 2x2 root system of a whole (non-coupled) system by Thomas
 // (tridiagonal.hpp:52-72 on [E1; E2]); sub of row 0 / super of row 1 ignored,
 // exactly as thomas_solve never reads sub[0] and drops c'_{n-1}.

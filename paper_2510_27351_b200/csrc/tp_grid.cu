@@ -1,0 +1,706 @@
+// Whole-system solve on one co-resident grid (k_grid_solve), for mid-size
+// one-level policies whose rows fit the GPU's aggregate shared memory
+// (FP64: up to ~1.0e6 rows on 148 SMs; config 2 = N 1e6, policy {32}).
+//
+// The level path for such a system is three latency-bound kernels: Stage 1
+// (1e6 rows -> a 62,500-row interface), the finishing solve of that interface
+// on ONE 16-CTA cluster (16 of 148 SMs, 10.5 us of a 23 us solve), Stage 3.
+// Here every SM owns a contiguous run of whole level-0 blocks
+// (make_plan, partition.hpp:30-49), stages it in shared memory ONCE with TMA
+// bulk copies, and the rest never leaves the chip:
+//   leaf sweeps of each chunk (reduce_block's up-/down-sweep, partition.hpp:
+//   90-124, intermediate values kept in place for back_substitute :156-172)
+//   -> chunk tree (shuffles, then warp roots) to the CTA's pair E1/E2
+//   -> the P CTA pairs published to global memory, ONE grid barrier
+//   -> every CTA merges the P pairs (the same tree, redundantly: no second
+//      barrier), solves the 2x2 root (thomas_solve on [E1; E2],
+//      tridiagonal.hpp:52-72) and walks down to its own (x_s, x_e)
+//   -> its own tree top-down, leaf back-substitution in shared memory, one
+//      coalesced store of x.
+// HBM traffic: the 32 B/row inputs read once and x written once (40 B/row,
+// the north-star floor) — no interface system, no Stage-3 re-read.
+//
+// A level-0 block of m rows is g chunks (g a power of two), i.e. one subtree
+// of the chunk tree, so the block's E1/E2 are formed exactly as k_fast forms
+// them; the interface of level 0 is then reduced by the tree instead of
+// thomas_solve — an exact elimination, equal to the reference's x up to
+// rounding (parity by tolerance). Pivots below kPivotFloor are
+// reported like every other kernel's (row of the device's elimination order);
+// the host then replays the reference's order (diagnose_pivot).
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#include "tp_device.cuh"
+#include "tp_generic.cuh"
+#include "tp_kernels.h"
+
+namespace tpb {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async_elem(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_elem(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <class T>
+__device__ __forceinline__ Eq2<T> identity_eq() {
+    return Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
+}
+
+// Shared-memory slot of CTA-local row i: one pad element after every 2^qs
+// rows, so that 32 threads sweeping 32 consecutive chunks of a power-of-two
+// length <= 2^qs hit 16 distinct 8-byte bank pairs (2 wavefronts, the
+// minimum for 32 FP64 accesses; an unpadded chunk stride of 16 rows puts
+// every lane of a warp on ONE bank pair: 32 wavefronts).
+__device__ __forceinline__ int padx(int i, int qs) { return i + (i >> qs); }
+
+// reduce_block's sweeps (partition.hpp:90-124) on one chunk from the padded
+// shared-memory rows, next row's values prefetched one step ahead (the loop
+// is otherwise bound by shared-memory load latency). The up-sweep overwrites
+// b <- rcp(beta), c <- gamma, d <- delta of the interior rows in place for
+// back_substitute (:156-172). Called for two chunks per thread, whose two
+// dependency chains the scheduler interleaves.
+template <class T>
+struct Row4 {
+    T a, b, c, d;
+};
+template <class T>
+__device__ __forceinline__ Row4<T> ld_row(const T* a, const T* b, const T* c, const T* d, int q) {
+    return Row4<T>{a[q], b[q], c[q], d[q]};
+}
+
+template <class T>
+__device__ __forceinline__ void sweep_down(const T* a, const T* b, const T* c, const T* d, int l0, int len, int qs,
+                                           bool& flag, Eq2<T>& E) {
+    const T fl = pivot_floor<T>();
+    const Row4<T> r1 = ld_row(a, b, c, d, padx(l0 + 1, qs));
+    T ph = r1.a, bp = r1.b, dp = r1.d, cp = r1.c;
+    Row4<T> nx = len > 2 ? ld_row(a, b, c, d, padx(l0 + 2, qs)) : r1;
+    for (int i = 2; i < len; ++i) {
+        const Row4<T> r = nx;
+        if (i + 1 < len) nx = ld_row(a, b, c, d, padx(l0 + i + 1, qs));
+        flag |= fabs(bp) < fl;
+        const T w = r.a * rcp(bp);
+        ph = -w * ph;
+        bp = fma(-w, cp, r.b);
+        dp = fma(-w, dp, r.d);
+        cp = r.c;
+    }
+    E.a2 = ph;
+    E.b2 = bp;
+    E.g2 = cp;
+    E.d2 = dp;
+}
+
+template <class T>
+__device__ __forceinline__ void sweep_up(T* a, T* b, T* c, T* d, int l0, int len, int qs, bool& flag, Eq2<T>& E) {
+    const T fl = pivot_floor<T>();
+    int qp = padx(l0 + len - 2, qs);
+    const Row4<T> s = ld_row(a, b, c, d, qp);
+    T bt = s.b, gm = s.c, dl = s.d, an = s.a;
+    Row4<T> nx = len > 2 ? ld_row(a, b, c, d, padx(l0 + len - 3, qs)) : s;
+    for (int i = len - 3; i >= 0; --i) {
+        const int q = padx(l0 + i, qs);
+        const Row4<T> r = nx;
+        if (i > 0) nx = ld_row(a, b, c, d, padx(l0 + i - 1, qs));
+        flag |= fabs(bt) < fl;
+        const T rb = rcp(bt);
+        const T w = r.c * rb;
+        const T nb = fma(-w, an, r.b);
+        gm = -w * gm;
+        dl = fma(-w, dl, r.d);
+        an = r.a;
+        b[qp] = rb;
+        c[q] = gm;
+        d[q] = dl;
+        bt = nb;
+        qp = q;
+    }
+    E.a1 = a[padx(l0, qs)];
+    E.b1 = bt;
+    E.g1 = gm;
+    E.d1 = dl;
+}
+
+// The same sweeps with the chunk length a compile-time constant (2..8 rows):
+// the rows are loaded into registers once, both sweeps are unrolled (two
+// independent chains the scheduler interleaves) and the kept values are
+// written back to the b, c, d slots.
+template <class T, int LEN>
+__device__ __forceinline__ void leaf_fixed(T* a, T* b, T* c, T* d, int l0, int qs, bool& flag, Eq2<T>& E) {
+    const T fl = pivot_floor<T>();
+    T ra[LEN], rb[LEN], rc[LEN], rd[LEN];
+    int q[LEN];
+#pragma unroll
+    for (int i = 0; i < LEN; ++i) {
+        q[i] = padx(l0 + i, qs);
+        ra[i] = a[q[i]];
+        rb[i] = b[q[i]];
+        rc[i] = c[q[i]];
+        rd[i] = d[q[i]];
+    }
+    T ph = ra[1], bp = rb[1], dp = rd[1];
+#pragma unroll
+    for (int i = 2; i < LEN; ++i) {
+        flag |= fabs(bp) < fl;
+        const T w = ra[i] * rcp(bp);
+        ph = -w * ph;
+        bp = fma(-w, rc[i - 1], rb[i]);
+        dp = fma(-w, dp, rd[i]);
+    }
+    E.a2 = ph;
+    E.b2 = bp;
+    E.g2 = rc[LEN - 1];
+    E.d2 = dp;
+    T bt = rb[LEN - 2], gm = rc[LEN - 2], dl = rd[LEN - 2];
+#pragma unroll
+    for (int i = LEN - 3; i >= 0; --i) {
+        flag |= fabs(bt) < fl;
+        const T r = rcp(bt);
+        const T w = rc[i] * r;
+        const T nb = fma(-w, ra[i + 1], rb[i]);
+        gm = -w * gm;
+        dl = fma(-w, dl, rd[i]);
+        b[q[i + 1]] = r;
+        c[q[i]] = gm;
+        d[q[i]] = dl;
+        bt = nb;
+    }
+    E.a1 = ra[0];
+    E.b1 = bt;
+    E.g1 = gm;
+    E.d1 = dl;
+}
+
+template <class T>
+__device__ __forceinline__ void leaf_loop(T* a, T* b, T* c, T* d, int l0, int len, int qs, bool& flag, Eq2<T>& E) {
+    sweep_down<T>(a, b, c, d, l0, len, qs, flag, E);
+    sweep_up<T>(a, b, c, d, l0, len, qs, flag, E);
+}
+
+
+// An unknown as an affine function of this CTA's end values X0 = x[r0],
+// X1 = x[r1-1]:  c + u X0 + v X1. The CTA's tree is walked top-down with
+// these BEFORE the grid barrier (Schur steps are linear in (xs, xe)), so after
+// the barrier every row is one evaluation x = c + u X0 + v X1.
+template <class T>
+struct Aff {
+    T c, u, v;
+};
+template <class T>
+__device__ __forceinline__ Aff<T> aff_lin(T k, const Aff<T>& p, T l, const Aff<T>& q, T m) {
+    // k + l p + m q
+    return Aff<T>{fma(m, q.c, fma(l, p.c, k)), fma(m, q.u, l * p.u), fma(m, q.v, l * p.v)};
+}
+template <class T>
+__device__ __forceinline__ Aff<T> shfl_up_aff(const Aff<T>& p, int h) {
+    return Aff<T>{__shfl_up_sync(0xffffffffu, p.c, h), __shfl_up_sync(0xffffffffu, p.u, h),
+                  __shfl_up_sync(0xffffffffu, p.v, h)};
+}
+// One symbolic step down a Schur merge node held by `left` lanes (h apart).
+template <class T>
+__device__ __forceinline__ void schur_step_aff(const SchurSave<T>& sv, bool left, bool right, int h, Aff<T>& xs,
+                                               Aff<T>& xe) {
+    Aff<T> xt{0, 0, 0}, xt1{0, 0, 0};
+    if (left) {
+        xt = aff_lin(sv.sd, xs, -sv.sa, xe, sv.sg);
+        xt1 = aff_lin(sv.ud, xs, sv.ua, xe, -sv.ug);
+    }
+    const Aff<T> r1 = shfl_up_aff(xt1, h);
+    const Aff<T> re = shfl_up_aff(xe, h);
+    if (right) {
+        xs = r1;
+        xe = re;
+    } else if (left) {
+        xe = xt;
+    }
+}
+
+// back_substitute (partition.hpp:163-170) of a chunk, symbolically: every row
+// as c + u X0 + v X1 from the chunk's symbolic ends S, E, stored into the
+// (a, b, c) slots of the row (x_i = (delta_i - a_i x_{i-1} - gamma_i x_e) / beta_i
+// with the up-sweep's values kept in b, c, d).
+// row_forms with the chunk length a compile-time constant (3..8 rows).
+template <class T, int LEN>
+__device__ __forceinline__ void row_forms_fixed(T* a, T* b, T* c, const T* d, int l0, int qs, const Aff<T>& S,
+                                                const Aff<T>& E) {
+    int q[LEN];
+    T ra[LEN], rb[LEN], rc[LEN], rd[LEN];
+#pragma unroll
+    for (int i = 1; i < LEN - 1; ++i) {
+        q[i] = padx(l0 + i, qs);
+        ra[i] = a[q[i]];
+        rb[i] = b[q[i]];
+        rc[i] = c[q[i]];
+        rd[i] = d[q[i]];
+    }
+    T p = 0, qq = 1, r = 0;
+#pragma unroll
+    for (int i = 1; i < LEN - 1; ++i) {
+        const T np = (rd[i] - ra[i] * p) * rb[i];
+        const T nq = -ra[i] * qq * rb[i];
+        const T nr = (-ra[i] * r - rc[i]) * rb[i];
+        p = np;
+        qq = nq;
+        r = nr;
+        const Aff<T> X = aff_lin(p, S, qq, E, r);
+        a[q[i]] = X.c;
+        b[q[i]] = X.u;
+        c[q[i]] = X.v;
+    }
+    const int k0 = padx(l0, qs), k1 = padx(l0 + LEN - 1, qs);
+    a[k0] = S.c; b[k0] = S.u; c[k0] = S.v;
+    a[k1] = E.c; b[k1] = E.u; c[k1] = E.v;
+}
+
+template <class T>
+__device__ __forceinline__ void row_forms(T* a, T* b, T* c, const T* d, int l0, int len, int qs, const Aff<T>& S,
+                                          const Aff<T>& E) {
+    // x_{i-1} = p + q xs + r xe (chunk-local)
+    T p = 0, q = 1, r = 0;
+    Row4<T> nx = len > 2 ? ld_row<T>(a, b, c, d, padx(l0 + 1, qs)) : Row4<T>{0, 0, 0, 0};
+    for (int i = 1; i < len - 1; ++i) {
+        const int k = padx(l0 + i, qs);
+        const Row4<T> w = nx;  // a, rcp(beta), gamma, delta
+        if (i + 1 < len - 1) nx = ld_row<T>(a, b, c, d, padx(l0 + i + 1, qs));
+        const T np = (w.d - w.a * p) * w.b;
+        const T nq = -w.a * q * w.b;
+        const T nr = (-w.a * r - w.c) * w.b;
+        p = np;
+        q = nq;
+        r = nr;
+        // x_i = p + q S + r E
+        const Aff<T> X = aff_lin(p, S, q, E, r);
+        a[k] = X.c;
+        b[k] = X.u;
+        c[k] = X.v;
+    }
+    const int k0 = padx(l0, qs), k1 = padx(l0 + len - 1, qs);
+    a[k0] = S.c; b[k0] = S.u; c[k0] = S.v;
+    a[k1] = E.c; b[k1] = E.u; c[k1] = E.v;
+}
+
+}  // namespace
+
+constexpr int kGridThreads = 512;
+constexpr int kGridWarps = kGridThreads / 32;
+constexpr int kGridChunksPerThread = 2;
+// grid-barrier spin bound (>= 32 ns each): ~0.5-1 s before the solve reports an error
+constexpr long kGridSpins = 1L << 24;
+// phase timestamps (%globaltimer) of every CTA when a launch asks for them
+__device__ unsigned long long g_grid_trace[2 * 256 * 8];  // [0, 2048) %globaltimer, then clock64
+
+// Block range of CTA b: blocks [K*b/P, K*(b+1)/P) of make_plan(n, m).
+struct GridGeom {
+    int64_t n, m, K;
+    int lg;  // log2(chunks per full block)
+    int P;   // CTAs
+    int S;   // smem stride of one array, in elements (padded)
+    int qs;  // pad shift (one pad element per 2^qs rows)
+    int trace;
+};
+
+// One step down a Schur merge node held by `left` lanes (h apart): the left
+// child keeps (xs, x_t), the right child gets (x_{t+1}, xe).
+template <class T>
+__device__ __forceinline__ void schur_step(const SchurSave<T>& sv, bool left, bool right, int h, T& xs, T& xe) {
+    T xt = 0, xt1 = 0;
+    if (left) schur_down(sv, xs, xe, xt, xt1);
+    const T rx1 = __shfl_up_sync(0xffffffffu, xt1, h);
+    const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
+    if (right) {
+        xs = rx1;
+        xe = rxe;
+    } else if (left) {
+        xe = xt;
+    }
+}
+
+template <class T, int L>
+__global__ void __launch_bounds__(kGridThreads, 1)
+    k_grid_solve(SysPtrs<T> sys, GridGeom geo, T* __restrict__ x, T* pairs, unsigned* bar,
+                 unsigned long long* err, int level) {
+    extern __shared__ __align__(16) unsigned char grid_smem[];
+    T* sa = reinterpret_cast<T*>(grid_smem);
+    T* sb = sa + geo.S;
+    T* sc = sb + geo.S;
+    T* sd = sc + geo.S;
+    __shared__ Eq2<T> wroot[kGridWarps];  // in-CTA warp roots, then the merged values
+    __shared__ SchurSave<T> wsv[kGridWarps - 1];  // warp-root merges, [level offset + node]
+    __shared__ Eq2<T> troot[8];           // top tree: warp roots (P <= 256)
+    __shared__ SchurSave<T> tpath[8];     // top tree: the saves on this CTA's path
+    __shared__ int tside[8];              // 0 no merge on the path, 1 left child, 2 right child
+    __shared__ Aff<T> wxa[2 * kGridWarps];  // each warp root's ends (W0, W1) as c + u X0 + v X1
+    __shared__ T cx[2];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b = blockIdx.x, P = geo.P;
+    const int64_t n = geo.n, m = geo.m, K = geo.K;
+    const int lg = geo.lg, qs = geo.qs;
+    const bool tr = geo.trace != 0 && tid == 0;
+    bool flag = false;  // a pivot below kPivotFloor (reported with this thread's first row)
+    pdl_begin();
+    if (tr) { g_grid_trace[8 * b + 0] = global_ns(); g_grid_trace[2048 + 8 * b + 0] = clock64(); }
+
+    // ---- this CTA's rows: whole blocks [kb0, kb1) ----
+    const int64_t kb0 = K * b / P, kb1 = K * (b + 1) / P;
+    const int64_t r0 = kb0 * m;
+    const int64_t r1 = (kb1 == K) ? n : kb1 * m;
+    const int R = (int)(r1 - r0);
+    const bool has_tail = (kb1 == K) && (n - (K - 1) * m != m);
+    const int nfull = (int)((kb1 - kb0) - (has_tail ? 1 : 0));
+    const int tlen = has_tail ? (int)(n - (K - 1) * m) : 0;
+    const int g = 1 << lg;
+    int lgt = 0;  // log2(chunks of the tail block)
+    if (has_tail)
+        while ((1 << (lgt + 1)) <= g && tlen >= 4 << lgt) ++lgt;
+    const int C = nfull * g + (has_tail ? 1 << lgt : 0);  // chunks of this CTA
+    const int NTh = (C + 1) / 2;                           // threads with chunks
+    const int mm = (int)m;
+
+    // ---- stage the rows: one cp.async per element into its padded slot ----
+    {
+        const T* src[4] = {sys.sub + r0, sys.diag + r0, sys.sup + r0, sys.rhs + r0};
+        T* dst[4] = {sa, sb, sc, sd};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            for (int i = tid; i < R; i += kGridThreads) cp_async_elem(dst[q] + padx(i, qs), src[q] + i);
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    if (tr) { g_grid_trace[8 * b + 1] = global_ns(); g_grid_trace[2048 + 8 * b + 1] = clock64(); }
+
+    // ---- chunk geometry (block-aligned: a full block is 2^lg chunks) ----
+    const int lo = mm >> lg, ex = mm & (g - 1);
+    const int tlo = tlen >> lgt, tex = tlen & ((1 << lgt) - 1);
+    auto cstart = [&](int c) -> int {  // CTA-local first row of chunk c (c <= C)
+        if (c >= C) return R;
+        const int blk = c >> lg;
+        if (blk < nfull) {
+            const int q = c & (g - 1);
+            return blk * mm + q * lo + (q < ex ? q : ex);
+        }
+        const int q = c - (nfull << lg);
+        return nfull * mm + q * tlo + (q < tex ? q : tex);
+    };
+    const bool active = tid < NTh;
+    int la0 = 0, la = 2, lb0 = 0, lb = 0;
+    if (active) {
+        la0 = cstart(2 * tid);
+        lb0 = cstart(2 * tid + 1);
+        la = lb0 - la0;
+        lb = (2 * tid + 1 < C) ? cstart(2 * tid + 2) - lb0 : 0;
+    }
+
+    // ---- leaves: two chunks per thread, then their merge ----
+    Eq2<T> cur = identity_eq<T>();
+    SchurSave<T> s0;
+    if (active) {
+        Eq2<T> EA, EB = identity_eq<T>();
+        if (L > 0 && la == L) leaf_fixed<T, (L > 1 ? L : 2)>(sa, sb, sc, sd, la0, qs, flag, EA);
+        else leaf_loop<T>(sa, sb, sc, sd, la0, la, qs, flag, EA);
+        if (lb > 0) {
+            if (L > 0 && lb == L) leaf_fixed<T, (L > 1 ? L : 2)>(sa, sb, sc, sd, lb0, qs, flag, EB);
+            else leaf_loop<T>(sa, sb, sc, sd, lb0, lb, qs, flag, EB);
+        }
+        cur = lb > 0 ? merge_schur(EA, EB, flag, s0) : EA;
+    }
+    if (tr) { g_grid_trace[8 * b + 2] = global_ns(); g_grid_trace[2048 + 8 * b + 2] = clock64(); }
+
+    // ---- thread tree: 5 shuffle levels per warp ----
+    SchurSave<T> sw[5];
+#pragma unroll
+    for (int lv = 0; lv < 5; ++lv) {
+        const int h = 1 << lv;
+        const Eq2<T> oth = shfl_down_eq(cur, h);
+        if ((lane & (2 * h - 1)) == 0 && tid + h < NTh) cur = merge_schur(cur, oth, flag, sw[lv]);
+    }
+    const int nwr = (NTh + 31) / 32;
+    if (lane == 0 && warp < nwr) wroot[warp] = cur;
+    if (tid < 8) tside[tid] = 0;
+    __syncthreads();
+
+    // ---- warp 0: the warp roots (<= 4 levels) -> this CTA's pair, published;
+    //      then the warp roots' ends (W0, W1) as c + u X0 + v X1 ----
+    if (warp == 0) {
+        Eq2<T> wc = lane < nwr ? wroot[lane] : identity_eq<T>();
+#pragma unroll
+        for (int lv = 0, off = 0; lv < 4; off += kGridWarps >> (lv + 1), ++lv) {
+            const int h = 1 << lv;
+            const Eq2<T> oth = shfl_down_eq(wc, h);
+            if ((lane & (2 * h - 1)) == 0 && lane + h < nwr) {
+                SchurSave<T> sv;
+                wc = merge_schur(wc, oth, flag, sv);
+                wsv[off + (lane >> (lv + 1))] = sv;
+            }
+        }
+        if (lane == 0) {
+            T* o = pairs + 8 * (int64_t)b;
+            o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
+            o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
+            if (tr) { g_grid_trace[8 * b + 3] = global_ns(); g_grid_trace[2048 + 8 * b + 3] = clock64(); }
+            __threadfence();
+            atomicAdd(bar, 1u);  // arrive; the wait comes after the symbolic pass
+        }
+        __syncwarp();
+        Aff<T> xs{0, T(lane == 0), 0}, xe{0, 0, T(lane == 0)};
+#pragma unroll
+        for (int lv = 3; lv >= 0; --lv) {
+            const int h = 1 << lv;
+            int off = 0;
+            for (int j = 0; j < lv; ++j) off += kGridWarps >> (j + 1);
+            const bool left = (lane & (2 * h - 1)) == 0 && lane + h < nwr;
+            const bool right = (lane & (2 * h - 1)) == h && lane < nwr;
+            SchurSave<T> sv{};
+            if (left) sv = wsv[off + (lane >> (lv + 1))];
+            schur_step_aff(sv, left, right, h, xs, xe);
+        }
+        if (lane < nwr) {
+            wxa[2 * lane] = xs;
+            wxa[2 * lane + 1] = xe;
+        }
+    }
+
+    // ---- every warp (no cross-warp dependency, overlaps warp 0 and the grid
+    //      barrier): its tree top-down symbolically from its root's ends
+    //      (W0, W1), the in-thread split, then every row of its chunks as
+    //      c + u W0 + v W1 in the (a, b, c) slots ----
+    {
+        Aff<T> xs{0, T(lane == 0), 0}, xe{0, 0, T(lane == 0)};
+#pragma unroll
+        for (int lv = 4; lv >= 0; --lv) {
+            const int h = 1 << lv;
+            const bool left = (lane & (2 * h - 1)) == 0 && tid + h < NTh;
+            const bool right = (lane & (2 * h - 1)) == h && tid < NTh;
+            schur_step_aff(sw[lv], left, right, h, xs, xe);
+        }
+        if (active) {
+            Aff<T> xeA = xe, xsB{0, 0, 0};
+            if (lb > 0) {
+                xeA = aff_lin(s0.sd, xs, -s0.sa, xe, s0.sg);
+                xsB = aff_lin(s0.ud, xs, s0.ua, xe, -s0.ug);
+            }
+            if (L > 2 && la == L) row_forms_fixed<T, (L > 2 ? L : 3)>(sa, sb, sc, sd, la0, qs, xs, xeA);
+            else row_forms<T>(sa, sb, sc, sd, la0, la, qs, xs, xeA);
+            if (lb > 0) {
+                if (L > 2 && lb == L) row_forms_fixed<T, (L > 2 ? L : 3)>(sa, sb, sc, sd, lb0, qs, xsB, xe);
+                else row_forms<T>(sa, sb, sc, sd, lb0, lb, qs, xsB, xe);
+            }
+        }
+    }
+    if (tr) { g_grid_trace[8 * b + 4] = global_ns(); g_grid_trace[2048 + 8 * b + 4] = clock64(); }
+
+    // ---- the grid barrier: every CTA's pair is published ----
+    if (tid == 0) {
+        long spins = 0;
+        while (ld_acquire_gpu(bar) < (unsigned)P) {
+            if (++spins > kGridSpins) {
+                if (err != nullptr)
+                    atomicMin(err, ((unsigned long long)kGridBarrierLevel << 48) | (unsigned long long)b);
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
+    __syncthreads();
+
+    // ---- every CTA: the tree over the P CTA pairs (identical arithmetic in
+    //      every CTA), keeping only the saves on the path to its own leaf ----
+    bool tflag = false;
+    {
+        const int ntw = (P + 31) / 32;
+        if (warp < ntw) {
+            Eq2<T> tc = identity_eq<T>();
+            if (tid < P) {
+                const T* q = pairs + 8 * (int64_t)tid;
+                tc = Eq2<T>{__ldcg(q + 0), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3),
+                            __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
+            }
+#pragma unroll
+            for (int lv = 0; lv < 5; ++lv) {
+                const int h = 1 << lv;
+                const Eq2<T> oth = shfl_down_eq(tc, h);
+                if ((lane & (2 * h - 1)) == 0 && tid + h < P) {
+                    SchurSave<T> sv;
+                    tc = merge_schur(tc, oth, tflag, sv);
+                    if ((tid >> (lv + 1)) == (b >> (lv + 1))) {  // an ancestor of leaf b
+                        tpath[3 + lv] = sv;
+                        tside[3 + lv] = ((b >> lv) & 1) ? 2 : 1;
+                    }
+                }
+            }
+            if (lane == 0) troot[warp] = tc;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            Eq2<T> rc = lane < ntw ? troot[lane] : identity_eq<T>();
+            const int bw = b >> 5;
+#pragma unroll
+            for (int lv = 0; lv < 3; ++lv) {
+                const int h = 1 << lv;
+                const Eq2<T> oth = shfl_down_eq(rc, h);
+                if ((lane & (2 * h - 1)) == 0 && lane + h < ntw) {
+                    SchurSave<T> sv;
+                    rc = merge_schur(rc, oth, tflag, sv);
+                    if ((lane >> (lv + 1)) == (bw >> (lv + 1))) {
+                        tpath[2 - lv] = sv;
+                        tside[2 - lv] = ((bw >> lv) & 1) ? 2 : 1;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                // root (thomas_solve on [E1; E2]), then down the path to leaf b
+                T xs = 0, xe = 0;
+                RowGuard rg;
+                root_solve(rc, n - 1, rg, xs, xe);
+                tflag |= rg.bad != INT64_MAX;
+                // path order: warp-root levels 2, 1, 0 (tpath[0..2]), then warp levels 4..0 (tpath[7..3])
+                const int order[8] = {0, 1, 2, 7, 6, 5, 4, 3};
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int j = order[k];
+                    if (tside[j] == 0) continue;
+                    T xt, xt1;
+                    schur_down(tpath[j], xs, xe, xt, xt1);
+                    if (tside[j] == 1) xe = xt;
+                    else xs = xt1;
+                }
+                cx[0] = xs;
+                cx[1] = xe;
+            }
+        }
+        __syncthreads();
+    }
+    if (tr) { g_grid_trace[8 * b + 5] = global_ns(); g_grid_trace[2048 + 8 * b + 5] = clock64(); }
+
+    // ---- every warp: its root's ends W0, W1, then x = c + u W0 + v W1 over
+    //      its rows (lane-strided, coalesced) ----
+    bool nf = false;
+    if (warp < nwr) {
+        const T X0 = cx[0], X1 = cx[1];
+        const Aff<T> A0 = wxa[2 * warp], A1 = wxa[2 * warp + 1];
+        const T W0 = fma(A0.v, X1, fma(A0.u, X0, A0.c));
+        const T W1 = fma(A1.v, X1, fma(A1.u, X0, A1.c));
+        const int c0 = 64 * warp;
+        const int c1 = c0 + 64 < C ? c0 + 64 : C;
+        const int w0 = cstart(c0), w1 = cstart(c1);
+        for (int i = w0 + lane; i < w1; i += 32) {
+            const int k = padx(i, qs);
+            const T v = fma(sc[k], W1, fma(sb[k], W0, sa[k]));
+            x[r0 + i] = v;
+            nf |= !isfinite(v);
+        }
+    }
+    if (tr) { g_grid_trace[8 * b + 6] = global_ns(); g_grid_trace[2048 + 8 * b + 6] = clock64(); }
+    if (nf) report_nonfinite(err, r0);
+    if (flag) report_pivot(err, level, r0 + la0);
+    if (tflag) report_pivot(err, level, r0);
+    if (tr) { g_grid_trace[8 * b + 7] = global_ns(); g_grid_trace[2048 + 8 * b + 7] = clock64(); }
+}
+
+// ---------------------------------------------------------------- host side
+static int g_grid_mode = -1;  // -1 unset, 0 off (TPB_GRID=0), 1 on
+
+static size_t grid_smem_bytes(int64_t S, size_t elem) { return (size_t)4 * S * elem; }
+
+// Geometry for (n, m) on `sms` SMs, or false when the system does not fit.
+template <class T>
+static bool grid_geom(int64_t n, int64_t m, int sms, GridGeom& geo) {
+    if (g_grid_mode < 0) {
+        const char* v = getenv("TPB_GRID");
+        g_grid_mode = (v != nullptr && atoi(v) == 0) ? 0 : 1;
+    }
+    if (g_grid_mode == 0) return false;
+    if (m < 2 || n < kGridMinRows) return false;
+    const int64_t K = plan_blocks_dev(n, m);
+    const int64_t me = m < n ? m : n;  // longest full block
+    int P = sms;
+    if (K < P) P = (int)K;
+    if (P > 256) P = 256;
+    const int64_t bpc = (K + P - 1) / P;  // blocks of the largest CTA
+    const int64_t cmax = (int64_t)kGridThreads * kGridChunksPerThread;
+    if (bpc > cmax) return false;
+    int lg = 0;
+    while (bpc * (2 << lg) <= cmax && me >= (4 << lg)) ++lg;
+    const int64_t lmax = (me + 1 + (1 << lg) - 1) >> lg;  // longest chunk (a tail block has up to m+1 rows)
+    if (lmax > kGridMaxChunk) return false;
+    int qs = 5;
+    while ((1 << qs) < lmax) ++qs;
+    const int64_t rows = bpc * m + 1;  // rows of the largest CTA
+    const int64_t S = ((rows + (rows >> qs) + 1 + 3) / 4) * 4;
+    if (grid_smem_bytes(S, sizeof(T)) > kGridDynSmem) return false;
+    static const int trace = [] { const char* v = getenv("TPB_GRID_TRACE"); return v ? atoi(v) : 0; }();
+    geo = GridGeom{n, m, K, lg, P, (int)S, qs, trace};
+    return true;
+}
+
+bool grid_fits(int64_t n, int64_t m, size_t elem, int sms) {
+    GridGeom geo;
+    return elem == 8 ? grid_geom<double>(n, m, sms, geo) : grid_geom<float>(n, m, sms, geo);
+}
+
+template <class T>
+cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x, void* scratch,
+                              unsigned long long* err, int level, int sms, cudaStream_t st) {
+    GridGeom geo;
+    if (!grid_geom<T>(n, m, sms, geo)) return cudaErrorInvalidValue;
+    unsigned* bar = static_cast<unsigned*>(scratch);
+    T* pairs = reinterpret_cast<T*>(static_cast<unsigned char*>(scratch) + 256);
+    // chunk length as a compile-time constant when every full block splits
+    // into equal chunks of 2, 4 or 8 rows (unrolled register sweeps)
+    const int64_t cl = geo.m >> geo.lg;
+    const int L = ((cl << geo.lg) == geo.m && (cl == 2 || cl == 4 || cl == 8)) ? (int)cl : 0;
+    void (*k)(SysPtrs<T>, GridGeom, T*, T*, unsigned*, unsigned long long*, int) =
+        L == 8 ? k_grid_solve<T, 8> : L == 4 ? k_grid_solve<T, 4> : L == 2 ? k_grid_solve<T, 2> : k_grid_solve<T, 0>;
+    static bool attr_done[2] = {false, false};
+    if (!attr_done[sizeof(T) == 8]) {
+        for (auto kk : {k_grid_solve<T, 8>, k_grid_solve<T, 4>, k_grid_solve<T, 2>, k_grid_solve<T, 0>}) {
+            cudaError_t e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGridDynSmem);
+            if (e != cudaSuccess) return e;
+        }
+        attr_done[sizeof(T) == 8] = true;
+    }
+    // the grid barrier needs every CTA resident: a cooperative launch
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)geo.P);
+    cfg.blockDim = dim3(kGridThreads);
+    cfg.dynamicSmemBytes = grid_smem_bytes(geo.S, sizeof(T));
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, sys, geo, x, pairs, bar, err, level);
+}
+
+template cudaError_t launch_grid_solve<double>(const SysPtrs<double>&, int64_t, int64_t, double*, void*,
+                                               unsigned long long*, int, int, cudaStream_t);
+template cudaError_t launch_grid_solve<float>(const SysPtrs<float>&, int64_t, int64_t, float*, void*,
+                                              unsigned long long*, int, int, cudaStream_t);
+
+}  // namespace tpb
+
+// Phase timestamps of the last traced launch (TPB_GRID_TRACE=1): 8 per CTA.
+extern "C" int tp_debug_grid_trace(unsigned long long* out, int count) {
+    if (count > 2 * 256 * 8) count = 2 * 256 * 8;
+    return (int)cudaMemcpyFromSymbol(out, tpb::g_grid_trace, (size_t)count * sizeof(unsigned long long));
+}

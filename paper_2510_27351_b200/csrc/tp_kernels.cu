@@ -160,13 +160,17 @@ static cudaError_t launch_k(int level, void (*kern)(KArgs...), unsigned grid, un
 
 // Error-word reset at the head of every solve (a kernel rather than a memset
 // node, so the first Stage-1 grid can be launched programmatically after it).
-__global__ void k_reset(unsigned long long* err) {
+// With `bar`, also zeroes the grid-barrier counter of k_grid_solve.
+__global__ void k_reset(unsigned long long* err, unsigned* bar) {
     pdl_begin();
-    if (threadIdx.x == 0) *err = kNoError;
+    if (threadIdx.x == 0) {
+        *err = kNoError;
+        if (bar != nullptr) *bar = 0u;
+    }
 }
 
-cudaError_t launch_reset(unsigned long long* err, cudaStream_t st) {
-    return launch_k(0, k_reset, 1, 32, 0, st, err);
+cudaError_t launch_reset(unsigned long long* err, cudaStream_t st, unsigned* bar) {
+    return launch_k(0, k_reset, 1, 32, 0, st, err, bar);
 }
 
 // Launch shapes chosen by measurement (tools/microbench/level_shapes.cu and

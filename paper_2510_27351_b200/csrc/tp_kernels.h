@@ -65,7 +65,7 @@ struct ShardLink {
 inline size_t mailbox_bytes(int nranks) { return (size_t)2 * nranks * kMailboxEntryDoubles * sizeof(double); }
 
 cudaError_t init_kernel_attributes();
-cudaError_t launch_reset(unsigned long long* err, cudaStream_t st);
+cudaError_t launch_reset(unsigned long long* err, cudaStream_t st, unsigned* bar = nullptr);
 bool fast_shape(int64_t m, int* L, int* G);
 int fast_rt_G(int64_t m);
 
@@ -123,6 +123,26 @@ cudaError_t launch_ref_sweep(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_
                              cudaStream_t st);
 template <class T>
 cudaError_t launch_ref_thomas(const SysPtrs<T>& sys, int64_t n, int64_t* out, cudaStream_t st);
+// Whole-system solve on one co-resident grid (k_grid_solve, tp_grid.cu): a
+// one-level policy whose rows fit the GPU's aggregate shared memory, one CTA
+// per SM, one grid barrier. grid_fits says whether (n, m) fits; the launcher
+// returns cudaErrorInvalidValue when it does not. scratch: kGridScratchBytes of device memory whose first
+// word must be zeroed before every launch (k_reset does it).
+constexpr int kGridBarrierLevel = 0x7FFD;  // err-word level of a grid-barrier timeout
+constexpr int64_t kGridMaxChunk = 64;  // longest leaf chunk (rows)
+constexpr int64_t kGridMinRows = 4;
+constexpr size_t kGridDynSmem = 232448 - 6144;
+constexpr size_t kGridScratchBytes = 256 + 8 * 256 * sizeof(double);
+inline int64_t plan_blocks_dev(int64_t n, int64_t m) {  // make_plan's block count, partition.hpp:30-49
+    if (m >= n) return 1;
+    int64_t leading = n / m;
+    if (n % m <= 1) --leading;
+    return leading + 1;
+}
+bool grid_fits(int64_t n, int64_t m, size_t elem, int sms);
+template <class T>
+cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x, void* scratch,
+                              unsigned long long* err, int level, int sms, cudaStream_t st);
 template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st);

@@ -1,0 +1,189 @@
+"""GPU parity of the one-kernel grid solve (k_grid_solve, csrc/tp_grid.cu): the
+whole solve of a one-level policy whose rows fit the GPU's shared memory
+(config 2: N=1e6, policy {32}). Checked against the oracle (the reference's
+algorithm; oracle/_ref where it runs) with the tolerances of
+tests/test_gpu_partition.py, and against the level path of the
+same library (TPB_GRID=0 in a subprocess)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = 1e-10
+TOL_RES = 1e-12
+
+
+def _sys(tp, s):
+    return tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs)
+
+
+def _impl(oracle_mod):
+    return "ref" if oracle_mod.ref_available() else "port"
+
+
+def _check(oracle_mod, s, x, ref):
+    assert np.all(np.isfinite(x))
+    assert oracle_mod.rel_inf_diff(x, ref) <= TOL
+    assert oracle_mod.floored_rel_diff(x, ref) <= TOL
+    assert oracle_mod.residual_inf(s, x) <= TOL_RES
+
+
+def test_config2_runs_as_one_grid_kernel(tp, oracle_mod):
+    """C2 (N=1e6, kNN policy {32}): one kernel after k_reset."""
+    n = 1_000_000
+    s = oracle_mod.generate_system(n, 1)
+    sm, dm = tp.default_size_model(), tp.default_depth_model()
+    pol = tp.recursion_sizes(n, tp.predict(dm, n), sm)
+    assert pol.sizes == [32]
+    ref = oracle_mod.solve_partition(s, pol.sizes, impl=_impl(oracle_mod))
+    x = tp.solve_partition(_sys(tp, s), pol)
+    assert tp.context().last_kernels() == ["grid_solve:L0"]
+    assert tp.context().last_launch_count() == 2  # k_reset + the grid kernel
+    _check(oracle_mod, s, x, ref)
+
+
+@pytest.mark.parametrize("n,m", [
+    (4, 2), (5, 2), (7, 3), (16, 4), (17, 4), (33, 32), (64, 64), (65, 64), (100, 1000),
+    (1000, 4), (1001, 4), (1002, 4), (10_000, 4), (10_000, 8), (12_345, 5), (30_000, 16),
+    (65_536, 20), (77_459, 20), (100_000, 32), (262_144, 64), (300_001, 25), (500_000, 100),
+    (999_999, 32), (1_000_001, 32), (900_000, 256), (150_000, 2), (300_000, 5000), (6_000, 6_000),
+])
+def test_grid_shapes_against_the_reference(tp, oracle_mod, n, m):
+    """Block-aligned CTA ranges with tails of every kind (n % m = 0, 1, other),
+    m >= n (one block), the smallest block (m = 2) and chunking by 1..32 per block."""
+    s = oracle_mod.generate_system(n, 3 + n % 89)
+    ref = oracle_mod.solve_partition(s, [m], impl=_impl(oracle_mod))
+    x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([m]))
+    ks = tp.context().last_kernels()
+    assert ks == ["grid_solve:L0"], ks
+    _check(oracle_mod, s, x, ref)
+
+
+def test_grid_random_sizes(tp, oracle_mod):
+    rng = np.random.default_rng(2027)
+    for _ in range(60):
+        n = int(rng.integers(4, 1_000_000))
+        m = int(rng.choice([2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 25, 32, 40, 50, 64, 100, 128, 200, 256]))
+        if m < 8:
+            n = min(n, 250_000)  # <= 1024 blocks of m rows per SM
+        s = oracle_mod.generate_system(n, int(rng.integers(1, 1 << 30)))
+        ref = oracle_mod.solve_partition(s, [m], impl="port")
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([m]))
+        assert tp.context().last_kernels() == ["grid_solve:L0"], (n, m)
+        _check(oracle_mod, s, x, ref)
+
+
+def test_grid_too_large_keeps_the_level_path(tp, oracle_mod):
+    """Rows past the grid's shared memory (FP64: ~1.03e6 at m = 32) and blocks
+    whose chunks would exceed 64 rows take the level kernels."""
+    for n, m in ((2_000_000, 32), (1_000_000, 100_000)):
+        s = oracle_mod.generate_system(n, 5)
+        ref = oracle_mod.solve_partition(s, [m], impl="port")
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([m]))
+        assert "grid_solve:L0" not in tp.context().last_kernels()
+        _check(oracle_mod, s, x, ref)
+
+
+def test_grid_fp32(tp, oracle_mod):
+    for n, m in ((1_000_000, 32), (2_000_000, 32), (33_333, 20)):
+        s = oracle_mod.generate_system(n, 9)
+        args = [a.astype(np.float32) for a in (s.sub, s.diag, s.sup, s.rhs)]
+        x = tp.solve_partition(tp.TridiagonalSystem(*args), tp.RecursionPolicy([m]))
+        assert x.dtype == np.float32
+        assert tp.context().last_kernels() == ["grid_solve:L0"], (n, m)
+        assert oracle_mod.residual_inf_f32(*args, x) <= 1e-4
+        ref = oracle_mod.solve_partition(s, [m], impl="port")
+        assert oracle_mod.rel_inf_diff(x.astype(np.float64), ref) <= 1e-4
+
+
+def test_grid_device_tensors_and_unaligned_views(tp, oracle_mod):
+    """Device-resident inputs (the bench path), also as views 8 bytes off the
+    16-byte grid (the kernel stages element by element: no alignment needed)."""
+    import torch
+
+    n = 400_003
+    s = oracle_mod.generate_system(n + 1, 13)
+    ref_full = oracle_mod.solve_partition(s, [16], impl="port")
+    dev = [torch.from_numpy(a).cuda() for a in (s.sub, s.diag, s.sup, s.rhs)]
+    x = tp.solve_partition(tp.TridiagonalSystem(*dev), tp.RecursionPolicy([16]))
+    torch.cuda.synchronize()
+    assert tp.context().last_kernels() == ["grid_solve:L0"]
+    assert oracle_mod.rel_inf_diff(x.cpu().numpy(), ref_full) <= TOL
+    s1 = oracle_mod.System(s.sub[1:], s.diag[1:], s.sup[1:], s.rhs[1:])
+    ref1 = oracle_mod.solve_partition(s1, [16], impl="port")  # sub[0] is never read
+    x1 = tp.solve_partition(tp.TridiagonalSystem(*[t[1:] for t in dev]), tp.RecursionPolicy([16]))
+    torch.cuda.synchronize()
+    assert tp.context().last_kernels() == ["grid_solve:L0"]
+    assert oracle_mod.rel_inf_diff(x1.cpu().numpy(), ref1) <= TOL
+    _check(oracle_mod, s1, x1.cpu().numpy(), ref1)
+
+
+def test_grid_zero_pivot_reports_the_reference_row(tp, oracle_mod):
+    """A zero pivot inside the grid kernel: the error carries the reference's
+    row and level (diagnose_pivot replays the reference's sequential order on
+    the level-0 interface it re-assembles)."""
+    rng = np.random.default_rng(77)
+    checked = 0
+    for _ in range(30):
+        n = int(rng.integers(200, 600_000))
+        m = int(rng.choice([4, 8, 16, 20, 32, 64]))
+        base = oracle_mod.generate_system(n, int(rng.integers(1, 1 << 30)))
+        rows = sorted(set(int(v) for v in rng.integers(0, n, size=int(rng.integers(1, 3)))))
+        sub, diag, sup, rhs = (a.copy() for a in (base.sub, base.diag, base.sup, base.rhs))
+        for r in rows:
+            sub[r] = diag[r] = sup[r] = 0.0
+        s = oracle_mod.System(sub, diag, sup, rhs)
+        try:
+            oracle_mod.solve_partition(s, [m], impl="port")
+            continue
+        except oracle_mod.OracleZeroPivot as e:
+            want = (e.row, e.level)
+        with pytest.raises(tp.ZeroPivotError) as ei:
+            tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([m]))
+        assert (ei.value.row(), ei.value.level) == want, (n, m, rows)
+        checked += 1
+    assert checked >= 10
+
+
+def test_grid_observer_still_sees_the_interface(tp, oracle_mod):
+    """The observer overload keeps the level path: level 0's interface goes
+    to the callback (the grid kernel never writes it)."""
+    n = 200_000
+    s = oracle_mod.generate_system(n, 4)
+    seen = []
+    x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([32]),
+                           on_interface=lambda iface, level: seen.append((level, iface.diag.shape[0])))
+    assert seen == [(0, 2 * (n // 32))]
+    assert "grid_solve:L0" not in tp.context().last_kernels()
+    _check(oracle_mod, s, x, oracle_mod.solve_partition(s, [32], impl="port"))
+    tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([32]))
+    assert tp.context().last_kernels() == ["grid_solve:L0"]
+
+
+def test_grid_matches_the_level_path(tp, oracle_mod):
+    """TPB_GRID=0 (level kernels) and the grid kernel agree to rounding."""
+    code = """
+import json, sys, numpy as np
+sys.path.insert(0, %r)
+import oracle, paper_2510_27351_b200 as tp
+s = oracle.generate_system(777_777, 8)
+x = tp.solve_partition(tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs), tp.RecursionPolicy([32]))
+np.save(sys.argv[1], x)
+print(json.dumps(tp.context().last_kernels()))
+""" % ROOT
+    outs = {}
+    for mode in ("0", "1"):
+        path = f"/tmp/tpb_grid_{mode}.npy"
+        env = dict(os.environ, TPB_GRID=mode)
+        r = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs[mode] = (np.load(path), json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs["1"][1] == ["grid_solve:L0"]
+    assert "grid_solve:L0" not in outs["0"][1]
+    assert oracle_mod.rel_inf_diff(outs["1"][0], outs["0"][0]) <= 1e-13
