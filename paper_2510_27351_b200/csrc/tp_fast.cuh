@@ -103,9 +103,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int c = lane % G;  // chunk index inside the block
     pdl_begin();
 
-    for (int64_t base = (int64_t)blockIdx.x * THREADS; base < nchunks;
-         base += (int64_t)gridDim.x * THREADS) {
-        const int64_t t = base + threadIdx.x;
+    // one chunk per thread: the launcher always sizes a full grid (no
+    // grid-stride loop, whose carried indices spilled at the register cap)
+    {
+        const int64_t t = (int64_t)blockIdx.x * THREADS + threadIdx.x;
         // warp-uniform liveness: groups never straddle the nchunks boundary
         const bool active = t < nchunks;
         const int64_t row0 = t * L;
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
 // k_fast shape (e.g. the sweep candidates 25, 35, 50, 100, 125, 250).
 // ===========================================================================
 template <class T, int LMAX, int G, int MODE>
-__global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
+__global__ void __launch_bounds__(128, (MODE == kStage1) ? 5 : 4)
     k_fast_rt(SysPtrs<T> sys, int64_t nblocks, int64_t m, IfacePtrs<T> out, const T* __restrict__ xi,
               T* __restrict__ x, unsigned long long* err, int level) {
     static_assert(32 % G == 0, "G must divide the warp");
@@ -162,9 +163,8 @@ __global__ void __launch_bounds__(128, (MODE == kStage1) ? 6 : 4)
     const int off = c * llo + (c < ext ? c : ext);
     pdl_begin();
 
-    for (int64_t base = (int64_t)blockIdx.x * THREADS; base < nchunks;
-         base += (int64_t)gridDim.x * THREADS) {
-        const int64_t t = base + threadIdx.x;
+    {  // one chunk per thread (full grid, as k_fast)
+        const int64_t t = (int64_t)blockIdx.x * THREADS + threadIdx.x;
         const bool active = t < nchunks;
         const int64_t blk = t / G;
         const int64_t row0 = blk * m + off;

@@ -175,13 +175,15 @@ cudaError_t launch_reset(unsigned long long* err, cudaStream_t st, unsigned* bar
 
 // Launch shapes chosen by measurement (tools/microbench/level_shapes.cu and
 // in-graph A/B runs on B200, N=1e8, m=64):
-// Stage 1  128 threads, <=80 regs (6 CTAs/SM), one chunk per thread (full grid)
+// Stage 1  128 threads, <=80 regs (6 CTAs/SM), one chunk per thread (full grid);
+//          L = 8 chunks at <=96 regs (5 CTAs/SM): at 80 their leaf spilled
+//          40-48 bytes per thread
 // Stage 3  128 threads, <=128 regs (4 CTAs/SM), one chunk per thread (full
 //          grid: 1.2% faster in the solve graph than a persistent grid-stride)
 template <class T, int L, int G, int MODE, bool VEC>
 struct FastCfg {
     static constexpr int kThreads = 128;
-    static constexpr int kMinBlocks = (MODE == kStage1) ? 6 : 4;
+    static constexpr int kMinBlocks = (MODE == kStage1) ? (L == 8 ? 5 : 6) : 4;
     static void* fn() { return (void*)k_fast<T, L, G, MODE, VEC, kThreads, kMinBlocks>; }
 };
 
