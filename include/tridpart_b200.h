@@ -67,6 +67,10 @@ void tp_ctx_destroy(tp_ctx* ctx);
 tp_status tp_ctx_set_stream(tp_ctx* ctx, void* stream, tp_error* err);
 /* Disable/enable CUDA-graph capture of the device solve (default enabled). */
 tp_status tp_ctx_set_graphs(tp_ctx* ctx, int32_t enabled, tp_error* err);
+/* One-kernel grid solve (k_grid_solve) of one-level policies that fit the
+ * GPU's shared memory: enabled (default 1; env TPB_GRID) for n >= min_rows
+ * (default 80000, env TPB_GRID_MIN; below it the level path is faster). */
+tp_status tp_ctx_set_grid(tp_ctx* ctx, int32_t enabled, int64_t min_rows, tp_error* err);
 /* Number of kernels the last solve on this context launched (0 if none). */
 int64_t tp_ctx_last_launch_count(const tp_ctx* ctx);
 /* Names ("kernel:Llevel", comma-separated) of the kernels of the last solve on

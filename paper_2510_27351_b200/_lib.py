@@ -34,7 +34,7 @@ OK, ZERO_PIVOT, INVALID_SIZE, DEPTH_OUT_OF_RANGE, EMPTY_TRAINING_SET, K_TOO_LARG
 MALFORMED_HEADER, BAD_NUMBER, IO, CUDA, INVALID_ARGUMENT, NCCL = 6, 7, 8, 9, 10, 11
 
 EXPORTS = [
-    "tp_abi_version", "tp_ctx_create", "tp_ctx_destroy", "tp_ctx_set_stream", "tp_ctx_set_graphs",
+    "tp_abi_version", "tp_ctx_create", "tp_ctx_destroy", "tp_ctx_set_stream", "tp_ctx_set_graphs", "tp_ctx_set_grid",
     "tp_ctx_last_launch_count", "tp_ctx_last_kernels", "tp_solve_partition_f64", "tp_solve_partition_f64_dev",
     "tp_check_device_error", "tp_solve_partition_observe_f64", "tp_thomas_solve_f64",
     "tp_residual_inf_f64_dev", "tp_shard_reduce_f64_dev", "tp_shard_finish_f64_dev",
@@ -64,6 +64,7 @@ def _load():
         "tp_ctx_destroy": (None, [vp]),
         "tp_ctx_set_stream": (C.c_int, [vp, vp, E]),
         "tp_ctx_set_graphs": (C.c_int, [vp, C.c_int32, E]),
+        "tp_ctx_set_grid": (C.c_int, [vp, C.c_int32, C.c_int64, E]),
         "tp_ctx_last_launch_count": (C.c_int64, [vp]),
         "tp_ctx_last_kernels": (C.c_int64, [vp, C.c_char_p, C.c_int64]),
         "tp_solve_partition_f64": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, _I64, C.c_int32, vp, E]),

@@ -250,6 +250,8 @@ struct tp_ctx {
     void* d_small = nullptr;              // shard scratch (x2 + gather scratch)
     void* d_grid = nullptr;               // k_grid_solve: barrier word + CTA pairs
     bool no_grid = false;                 // observer solves: keep the level path (interfaces in HBM)
+    bool grid_on = true;                  // tp_ctx_set_grid / TPB_GRID
+    int64_t grid_min = 80000;             // tp_ctx_set_grid / TPB_GRID_MIN
     // fused multi-GPU path (k_final<kShard>): own mailbox, peer links, epoch word
     void* mailbox = nullptr;
     int mailbox_ranks = 0;
@@ -292,16 +294,13 @@ namespace {
 using KernelHook = void (*)(void* user, const char* name);
 
 // k_grid_solve takes the whole solve of a one-level policy whose rows fit the
-// grid's shared memory (TPB_GRID=0 disables it; TPB_GRID_MIN sets the
-// smallest n it takes, default kGridDefaultMin).
-constexpr int64_t kGridDefaultMin = 4;
+// grid's shared memory, for n >= ctx->grid_min (tp_ctx_set_grid; env TPB_GRID,
+// TPB_GRID_MIN at context creation). Below ~8e4 rows the level path is faster:
+// measured in-graph spans, tools/ab_grid_span.sh.
 template <class T>
 bool use_grid(const tp_ctx* ctx, const Plan<T>& p) {
-    static const int64_t gmin = [] {
-        const char* v = getenv("TPB_GRID_MIN");
-        return v ? (int64_t)atoll(v) : kGridDefaultMin;
-    }();
-    if (ctx->no_grid || p.npol != 1 || p.levels.empty() || p.n0 < gmin || p.n0 < 4) return false;
+    if (!ctx->grid_on || ctx->no_grid || p.npol != 1 || p.levels.empty() || p.n0 < ctx->grid_min || p.n0 < 4)
+        return false;
     return tpb::grid_fits(p.n0, p.m0, sizeof(T), ctx->sms);
 }
 
@@ -1206,6 +1205,8 @@ tp_status tp_ctx_create(int32_t device, tp_ctx** out, tp_error* err) {
     if (e == cudaSuccess) e = cudaMalloc(&c->d_small, 4096);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_grid, tpb::kGridScratchBytes);
     if (e == cudaSuccess) e = cudaMemset(c->d_grid, 0, tpb::kGridScratchBytes);
+    if (const char* v = getenv("TPB_GRID")) c->grid_on = atoi(v) != 0;
+    if (const char* v = getenv("TPB_GRID_MIN")) c->grid_min = std::max<int64_t>(4, atoll(v));
     if (e == cudaSuccess) e = cudaMallocHost(&c->h_err, 64);
     if (e != cudaSuccess) {
         set_err(err, TP_ERR_CUDA, std::string("context allocation: ") + cudaGetErrorString(e));
@@ -1249,6 +1250,19 @@ tp_status tp_ctx_set_graphs(tp_ctx* ctx, int32_t enabled, tp_error* err) {
     clear_err(err);
     TP_NEED_CTX(ctx);
     ctx->graphs = enabled != 0;
+    return TP_OK;
+}
+
+tp_status tp_ctx_set_grid(tp_ctx* ctx, int32_t enabled, int64_t min_rows, tp_error* err) {
+    clear_err(err);
+    TP_NEED_CTX(ctx);
+    if (min_rows < 4) {
+        set_err(err, TP_ERR_INVALID_ARGUMENT, "min_rows must be >= 4");
+        return TP_ERR_INVALID_ARGUMENT;
+    }
+    if ((enabled != 0) != ctx->grid_on || min_rows != ctx->grid_min) drop_graphs(ctx);
+    ctx->grid_on = enabled != 0;
+    ctx->grid_min = min_rows;
     return TP_OK;
 }
 

@@ -617,18 +617,12 @@ __global__ void __launch_bounds__(kGridThreads, 1)
 }
 
 // ---------------------------------------------------------------- host side
-static int g_grid_mode = -1;  // -1 unset, 0 off (TPB_GRID=0), 1 on
 
 static size_t grid_smem_bytes(int64_t S, size_t elem) { return (size_t)4 * S * elem; }
 
 // Geometry for (n, m) on `sms` SMs, or false when the system does not fit.
 template <class T>
 static bool grid_geom(int64_t n, int64_t m, int sms, GridGeom& geo) {
-    if (g_grid_mode < 0) {
-        const char* v = getenv("TPB_GRID");
-        g_grid_mode = (v != nullptr && atoi(v) == 0) ? 0 : 1;
-    }
-    if (g_grid_mode == 0) return false;
     if (m < 2 || n < kGridMinRows) return false;
     const int64_t K = plan_blocks_dev(n, m);
     const int64_t me = m < n ? m : n;  // longest full block

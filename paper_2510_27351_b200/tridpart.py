@@ -146,6 +146,11 @@ class Context:
     def set_graphs(self, enabled: bool):
         _call(lib.tp_ctx_set_graphs, self.handle, 1 if enabled else 0)
 
+    def set_grid(self, enabled: bool = True, min_rows: int = 80_000):
+        """The one-kernel grid solve of one-level policies (k_grid_solve): on/off
+        and the smallest n it takes (below ~8e4 rows the level path is faster)."""
+        _call(lib.tp_ctx_set_grid, self.handle, 1 if enabled else 0, int(min_rows))
+
     def last_launch_count(self) -> int:
         return int(lib.tp_ctx_last_launch_count(self.handle))
 

@@ -19,6 +19,14 @@ TOL = 1e-10
 TOL_RES = 1e-12
 
 
+@pytest.fixture(autouse=True)
+def _grid_for_all_sizes(tp):
+    """Small systems too (the default threshold keeps n < 8e4 on the level path)."""
+    tp.context().set_grid(True, 4)
+    yield
+    tp.context().set_grid(True, 80_000)
+
+
 def _sys(tp, s):
     return tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs)
 
@@ -180,7 +188,7 @@ print(json.dumps(tp.context().last_kernels()))
     outs = {}
     for mode in ("0", "1"):
         path = f"/tmp/tpb_grid_{mode}.npy"
-        env = dict(os.environ, TPB_GRID=mode)
+        env = dict(os.environ, TPB_GRID=mode, TPB_GRID_MIN="4")
         r = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr
         outs[mode] = (np.load(path), json.loads(r.stdout.strip().splitlines()[-1]))

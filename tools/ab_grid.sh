@@ -1,6 +1,7 @@
 #!/bin/bash
 # A/B of the one-kernel grid solve (TPB_GRID) against the level path, for the
 # one-level policies at small and mid N; phase traces and in-graph timelines of C1/C2.
+export TPB_GRID_MIN=4
 for spec in "1e4 4" "1e4 8" "3e4 16" "1e5 32" "3e5 32" "1e6 32" "1e6 16" "1e6 64"; do
   set -- $spec
   for g in 0 1; do TPB_GRID=$g python tools/solve_time.py --n $1 --policy $2 --steps 300 --tag grid=$g; done

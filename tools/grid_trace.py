@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     os.environ.setdefault("TPB_GRID_TRACE", "1")
+    os.environ.setdefault("TPB_GRID_MIN", "4")
     import numpy as np
     import torch
 

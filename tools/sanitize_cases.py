@@ -9,7 +9,8 @@ Covers: k_fast (fixed shapes, both stages, vector and scalar loads), k_fast_rt
 (runtime chunk lengths), k_generic (tail blocks, m > 256), the fused deepest
 level + finishing solve (k_level_final_cl: cp.async staging, register and
 shared-memory sweeps, 16-CTA cluster), level 1 folded into level 0
-(k_fast_s1fold), the cluster and the
+(k_fast_s1fold), the one-kernel grid solve (k_grid_solve: cp.async
+staging into padded shared memory, cooperative grid barrier), the cluster and the
 single-CTA finishing solves (solve, sharded reduce / expand, the fused
 peer exchange on one rank), FP32, thomas_solve, the
 generator and the residual. Sizes are small so the sanitizer finishes in
@@ -43,6 +44,9 @@ def main():
         (40_000, [64, 7]),       # fused deepest level, generic sweeps (odd m)
         (160_000, [64, 10, 8]),  # level 1 folded into level 0 (k_fast_s1fold)
         (640_000, [64, 10, 32]), # levels 1 and 2 folded (FOLD2)
+        (100_000, [32]),         # one-kernel grid solve, 8-row chunks (k_grid_solve<T, 8>)
+        (150_001, [4]),          # grid solve, 2-row chunks, tail block (k_grid_solve<T, 2>)
+        (90_007, [20]),          # grid solve, uneven chunks (k_grid_solve<T, 0>, loop leaves)
     ]
     worst = 0.0
     for n, sizes in cases:
