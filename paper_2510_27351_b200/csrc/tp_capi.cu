@@ -293,15 +293,23 @@ namespace {
 
 using KernelHook = void (*)(void* user, const char* name);
 
-// k_grid_solve takes the whole solve of a one-level policy whose rows fit the
-// grid's shared memory, for n >= ctx->grid_min (tp_ctx_set_grid; env TPB_GRID,
-// TPB_GRID_MIN at context creation). Below ~8e4 rows the level path is faster:
-// measured in-graph spans, tools/ab_grid_span.sh.
+// k_grid_solve takes the rest of the solve from the shallowest plan level whose
+// system fits the grid's shared memory (k = 0: the whole solve, e.g. config 2;
+// k >= 1: the levels below Stage 1 of levels 0..k-1), for systems of
+// >= ctx->grid_min rows (tp_ctx_set_grid; env TPB_GRID, TPB_GRID_MIN at context
+// creation). Below ~8e4 rows the level path is faster: measured in-graph spans,
+// tools/ab_grid_span.sh. Returns the plan level, or -1.
 template <class T>
-bool use_grid(const tp_ctx* ctx, const Plan<T>& p) {
-    if (!ctx->grid_on || ctx->no_grid || p.npol != 1 || p.levels.empty() || p.n0 < ctx->grid_min || p.n0 < 4)
-        return false;
-    return tpb::grid_fits(p.n0, p.m0, sizeof(T), ctx->sms);
+int grid_level(const tp_ctx* ctx, const Plan<T>& p) {
+    if (!ctx->grid_on || ctx->no_grid) return -1;
+    for (size_t k = 0; k < p.levels.size(); ++k) {
+        const Level<T>& L = p.levels[k];
+        if (L.n < ctx->grid_min || L.n < 4) return -1;  // deeper levels are smaller still
+        // (a split level carries its level's original n and m: the grid takes
+        // the original blocks, long ones as many chunks)
+        if (tpb::grid_fits(L.n, L.m, sizeof(T), ctx->sms)) return (int)k;
+    }
+    return -1;
 }
 
 template <class T>
@@ -400,7 +408,7 @@ struct Runner {
     // or, for a one-level policy that fits the grid's shared memory, the one
     // co-resident kernel k_grid_solve (tp_grid.cu).
     void solve(const Plan<T>& p) {
-        const bool grid = use_grid(ctx, p);
+        const bool grid = grid_level(ctx, p) >= 0;
         check(tpb::launch_reset(ctx->d_err, st, grid ? static_cast<unsigned*>(ctx->d_grid) : nullptr));
         ++launches;  // k_reset: counted, not timed by the profile hook
         solve_body(p, tpb::kSolve, grid);
@@ -434,11 +442,14 @@ struct Runner {
     // exchange at the root of the deepest level (k_level_final_cl<kShard>) or
     // of the finishing solve (k_final<kShard>).
     void solve_body(const Plan<T>& p, int mode = tpb::kSolve, bool bar_zeroed = false) {
-        if (mode == tpb::kSolve && use_grid(ctx, p)) {
-            const Level<T>& L0 = p.levels[0];
+        const int gk = mode == tpb::kSolve ? grid_level(ctx, p) : -1;
+        if (gk >= 0) {  // Stage 1 down to level gk, the grid solve from there, Stage 3 up
+            stage1_down(p, (size_t)gk);
+            const Level<T>& G = p.levels[(size_t)gk];
             if (!bar_zeroed) check(cudaMemsetAsync(ctx->d_grid, 0, sizeof(unsigned), st));
-            check(tpb::launch_grid_solve<T>(L0.in, p.n0, p.m0, L0.x_out, ctx->d_grid, ctx->d_err, 0, ctx->sms, st));
-            after("grid_solve", 0);
+            check(tpb::launch_grid_solve<T>(G.in, G.n, G.m, G.x_out, ctx->d_grid, ctx->d_err, gk, ctx->sms, st));
+            after("grid_solve", gk);
+            for (int l = gk; l-- > 0;) stage(p.levels[(size_t)l], l, tpb::kStage3);
             return;
         }
         const size_t nl = p.levels.size();
@@ -730,8 +741,8 @@ tp_status diagnose_pivot(tp_ctx* ctx, int64_t dev_row, int32_t dev_level, tp_err
     bind_plan(p, SysPtrs<T>{(const T*)ls.in[0], (const T*)ls.in[1], (const T*)ls.in[2], (const T*)ls.in[3]},
               (T*)ls.x, ctx->ws);
     const cudaStream_t st = ctx->own;
-    if (use_grid(ctx, p)) {
-        // k_grid_solve keeps level 0's interface on chip: assemble it now
+    if (grid_level(ctx, p) >= 0) {
+        // k_grid_solve keeps its levels' interfaces on chip: assemble them now
         // (the same Stage-1 kernels and arithmetic as the level path)
         Runner<T> r{ctx, st};
         r.stage1_down(p, p.levels.size());

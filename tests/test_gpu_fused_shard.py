@@ -106,6 +106,7 @@ ks = []
 x = sharded.simulate_ranks_fused(s.sub, s.diag, s.sup, s.rhs, P, pol, kernels=ks)
 g = sharded.shard_granule(pol)
 single = []
+tp.context().set_grid(False)  # the level path: the sharded graph has no grid solve
 for r in range(P):
     lo, cnt = sharded.shard_bounds(n, P, r, g)
     sysr = tp.TridiagonalSystem(*(a[lo:lo + cnt].copy() for a in (s.sub, s.diag, s.sup, s.rhs)))

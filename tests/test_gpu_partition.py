@@ -592,6 +592,7 @@ def test_folded_level_one(tp, oracle_mod, n, sizes):
 
     from paper_2510_27351_b200._lib import TpError, lib
 
+    tp.context().set_grid(False)  # the level path (the grid solve would take these whole)
     sd = tp.generate_system(n, 5, device=True)
     x = torch.empty(n, dtype=torch.float64, device="cuda")
     sz = np.asarray(sizes, dtype=np.int64)
@@ -610,6 +611,7 @@ def test_folded_level_one(tp, oracle_mod, n, sizes):
     x32 = tp.solve_partition(
         tp.TridiagonalSystem(*(a.astype(np.float32) for a in (s.sub, s.diag, s.sup, s.rhs))), tp.RecursionPolicy(sizes))
     assert oracle_mod.rel_inf_diff(x32.astype(np.float64), ref) <= 1e-4
+    tp.context().set_grid(True)
 
 
 def test_folded_level_one_reports_zero_pivots(tp):
