@@ -352,7 +352,8 @@ def run_ours(args):
         from paper_2510_27351_b200._lib import TpError, lib
         sz = np.asarray(policy.sizes, dtype=np.int64)
         reps = 10
-        if sharded_mode:  # the sharded graph has no grid solve: keep the standalone run alike
+        share_gpu = os.environ.get("TPB_SHARE_GPU") == "1"
+        if sharded_mode and share_gpu:  # ranks sharing a GPU run no grid solve: keep the standalone run alike
             tp.context().set_grid(False)
         for _ in range(reps if args.prewarm > 0 else 1):
             kms = (C.c_float * 64)()
@@ -370,7 +371,7 @@ def run_ours(args):
                 nm = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
                 prof.setdefault(nm, []).append(kms[i])
         prof = {k: statistics.median(v) for k, v in prof.items()}
-        if sharded_mode:
+        if sharded_mode and share_gpu:
             tp.context().set_grid(True)
     per_rank = None
     if dist is not None:

@@ -404,6 +404,15 @@ struct Runner {
         after("final", (int)p.levels.size());
     }
 
+    // The plan level the grid solve takes in this mode, or -1. Sharded (FP64):
+    // not when a peer shares this GPU (every rank's grid kernel needs all SMs
+    // while it waits for the others' pairs).
+    int grid_level_for(const Plan<T>& p, int mode) const {
+        if (mode == tpb::kSolve) return grid_level(ctx, p);
+        if (mode == tpb::kShard && sizeof(T) == 8 && !ctx->link_shared) return grid_level(ctx, p);
+        return -1;
+    }
+
     // Whole solve: reset the error word, Stage 1 down, finish, Stage 3 up —
     // or, for a one-level policy that fits the grid's shared memory, the one
     // co-resident kernel k_grid_solve (tp_grid.cu).
@@ -442,13 +451,14 @@ struct Runner {
     // exchange at the root of the deepest level (k_level_final_cl<kShard>) or
     // of the finishing solve (k_final<kShard>).
     void solve_body(const Plan<T>& p, int mode = tpb::kSolve, bool bar_zeroed = false) {
-        const int gk = mode == tpb::kSolve ? grid_level(ctx, p) : -1;
+        const int gk = grid_level_for(p, mode);
         if (gk >= 0) {  // Stage 1 down to level gk, the grid solve from there, Stage 3 up
             stage1_down(p, (size_t)gk);
             const Level<T>& G = p.levels[(size_t)gk];
             if (!bar_zeroed) check(cudaMemsetAsync(ctx->d_grid, 0, sizeof(unsigned), st));
-            check(tpb::launch_grid_solve<T>(G.in, G.n, G.m, G.x_out, ctx->d_grid, ctx->d_err, gk, ctx->sms, st));
-            after("grid_solve", gk);
+            check(tpb::launch_grid_solve<T>(G.in, G.n, G.m, G.x_out, ctx->d_grid, ctx->d_err, gk, ctx->sms, st, mode,
+                                            mode == tpb::kShard ? &ctx->link : nullptr));
+            after(mode == tpb::kShard ? "grid_exchange" : "grid_solve", gk);
             for (int l = gk; l-- > 0;) stage(p.levels[(size_t)l], l, tpb::kStage3);
             return;
         }
@@ -487,9 +497,10 @@ struct Runner {
     // the deepest level fused with the finishing solve, Stage 3 up) with the
     // peer exchange and the top solve at the root of the deepest level.
     void shard_solve(const Plan<T>& p) {
-        check(tpb::launch_reset(ctx->d_err, st));
+        const bool grid = grid_level_for(p, tpb::kShard) >= 0;
+        check(tpb::launch_reset(ctx->d_err, st, grid ? static_cast<unsigned*>(ctx->d_grid) : nullptr));
         ++launches;  // k_reset: counted, not timed by the profile hook
-        solve_body(p, tpb::kShard);
+        solve_body(p, tpb::kShard, grid);
     }
     void shard_finish(const Plan<T>& p, const T* eq_all, int nranks, int rank) {
         T* x2 = static_cast<T*>(ctx->d_small);

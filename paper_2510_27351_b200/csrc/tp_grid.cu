@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include "tp_device.cuh"
+#include "tp_exchange.cuh"
 #include "tp_generic.cuh"
 #include "tp_kernels.h"
 
@@ -333,10 +334,15 @@ __device__ __forceinline__ void schur_step(const SchurSave<T>& sv, bool left, bo
     }
 }
 
-template <class T, int L>
+// MODE kSolve: the root pair is the whole system (thomas_solve on [E1; E2]).
+// MODE kShard: the root pair is this rank's shard; CTA 0 exchanges it with
+// every peer over peer memory (shard_exchange, tp_exchange.cuh), solves the
+// 2P-row top system and hands the shard's ends to the other CTAs through a
+// second arrival on the barrier counter.
+template <class T, int L, int MODE>
 __global__ void __launch_bounds__(kGridThreads, 1)
     k_grid_solve(SysPtrs<T> sys, GridGeom geo, T* __restrict__ x, T* pairs, unsigned* bar,
-                 unsigned long long* err, int level) {
+                 unsigned long long* err, int level, const __grid_constant__ ShardLink link) {
     extern __shared__ __align__(16) unsigned char grid_smem[];
     T* sa = reinterpret_cast<T*>(grid_smem);
     T* sb = sa + geo.S;
@@ -569,9 +575,37 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             if (lane == 0) {
                 // root (thomas_solve on [E1; E2]), then down the path to leaf b
                 T xs = 0, xe = 0;
-                RowGuard rg;
-                root_solve(rc, n - 1, rg, xs, xe);
-                tflag |= rg.bad != INT64_MAX;
+                if constexpr (MODE == kShard) {
+                    T* root = pairs + 8 * 256;  // the shard's (x_s, x_e), CTA 0 -> the others
+                    if (b == 0) {
+                        __shared__ double top_cm[2 * kMaxPeers], top_x[2 * kMaxPeers];
+                        RowGuard top_bad;
+                        int missing = -1;
+                        if (!shard_exchange(link, rc, top_cm, top_x, xs, xe, top_bad, missing) && err != nullptr)
+                            atomicMin(err, ((unsigned long long)kExchangeLevel << 48) | (unsigned long long)missing);
+                        report_pivot(err, level + 1, top_bad.bad);
+                        root[0] = xs;
+                        root[1] = xe;
+                        __threadfence();
+                        atomicAdd(bar, 1u);
+                    } else {
+                        long spins = 0;
+                        while (ld_acquire_gpu(bar) < (unsigned)P + 1u) {
+                            if (++spins > 2 * kExchangeSpins) {
+                                if (err != nullptr)
+                                    atomicMin(err, ((unsigned long long)kGridBarrierLevel << 48) | (unsigned long long)b);
+                                break;
+                            }
+                            __nanosleep(64);
+                        }
+                        xs = __ldcg(root);
+                        xe = __ldcg(root + 1);
+                    }
+                } else {
+                    RowGuard rg;
+                    root_solve(rc, n - 1, rg, xs, xe);
+                    tflag |= rg.bad != INT64_MAX;
+                }
                 // path order: warp-root levels 2, 1, 0 (tpath[0..2]), then warp levels 4..0 (tpath[7..3])
                 const int order[8] = {0, 1, 2, 7, 6, 5, 4, 3};
 #pragma unroll
@@ -651,23 +685,37 @@ bool grid_fits(int64_t n, int64_t m, size_t elem, int sms) {
     return elem == 8 ? grid_geom<double>(n, m, sms, geo) : grid_geom<float>(n, m, sms, geo);
 }
 
+template <class T, int MODE>
+using GridKernel = void (*)(SysPtrs<T>, GridGeom, T*, T*, unsigned*, unsigned long long*, int, const ShardLink);
+
+template <class T, int MODE>
+static GridKernel<T, MODE> grid_kernel(int L) {
+    return L == 8 ? k_grid_solve<T, 8, MODE> : L == 4 ? k_grid_solve<T, 4, MODE>
+           : L == 2 ? k_grid_solve<T, 2, MODE> : k_grid_solve<T, 0, MODE>;
+}
+
 template <class T>
 cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x, void* scratch,
-                              unsigned long long* err, int level, int sms, cudaStream_t st) {
+                              unsigned long long* err, int level, int sms, cudaStream_t st, int mode,
+                              const ShardLink* link) {
     GridGeom geo;
     if (!grid_geom<T>(n, m, sms, geo)) return cudaErrorInvalidValue;
+    if (mode == kShard && (sizeof(T) != 8 || link == nullptr || link->nranks < 1 || link->nranks > kMaxPeers))
+        return cudaErrorInvalidValue;  // the mailboxes carry FP64 pairs
     unsigned* bar = static_cast<unsigned*>(scratch);
     T* pairs = reinterpret_cast<T*>(static_cast<unsigned char*>(scratch) + 256);
     // chunk length as a compile-time constant when every full block splits
     // into equal chunks of 2, 4 or 8 rows (unrolled register sweeps)
     const int64_t cl = geo.m >> geo.lg;
     const int L = ((cl << geo.lg) == geo.m && (cl == 2 || cl == 4 || cl == 8)) ? (int)cl : 0;
-    void (*k)(SysPtrs<T>, GridGeom, T*, T*, unsigned*, unsigned long long*, int) =
-        L == 8 ? k_grid_solve<T, 8> : L == 4 ? k_grid_solve<T, 4> : L == 2 ? k_grid_solve<T, 2> : k_grid_solve<T, 0>;
     static bool attr_done[2] = {false, false};
     if (!attr_done[sizeof(T) == 8]) {
-        for (auto kk : {k_grid_solve<T, 8>, k_grid_solve<T, 4>, k_grid_solve<T, 2>, k_grid_solve<T, 0>}) {
-            cudaError_t e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGridDynSmem);
+        for (int l : {8, 4, 2, 0}) {
+            cudaError_t e = cudaFuncSetAttribute(grid_kernel<T, kSolve>(l), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kGridDynSmem);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(grid_kernel<T, kShard>(l), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kGridDynSmem);
             if (e != cudaSuccess) return e;
         }
         attr_done[sizeof(T) == 8] = true;
@@ -683,13 +731,15 @@ cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x,
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, sys, geo, x, pairs, bar, err, level);
+    const ShardLink none{};
+    if (mode == kShard) return cudaLaunchKernelEx(&cfg, grid_kernel<T, kShard>(L), sys, geo, x, pairs, bar, err, level, *link);
+    return cudaLaunchKernelEx(&cfg, grid_kernel<T, kSolve>(L), sys, geo, x, pairs, bar, err, level, none);
 }
 
 template cudaError_t launch_grid_solve<double>(const SysPtrs<double>&, int64_t, int64_t, double*, void*,
-                                               unsigned long long*, int, int, cudaStream_t);
+                                               unsigned long long*, int, int, cudaStream_t, int, const ShardLink*);
 template cudaError_t launch_grid_solve<float>(const SysPtrs<float>&, int64_t, int64_t, float*, void*,
-                                              unsigned long long*, int, int, cudaStream_t);
+                                              unsigned long long*, int, int, cudaStream_t, int, const ShardLink*);
 
 }  // namespace tpb
 

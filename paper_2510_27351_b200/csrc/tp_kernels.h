@@ -132,7 +132,7 @@ constexpr int kGridBarrierLevel = 0x7FFD;  // err-word level of a grid-barrier t
 constexpr int64_t kGridMaxChunk = 64;  // longest leaf chunk (rows)
 constexpr int64_t kGridMinRows = 4;
 constexpr size_t kGridDynSmem = 232448 - 6144;
-constexpr size_t kGridScratchBytes = 256 + 8 * 256 * sizeof(double);
+constexpr size_t kGridScratchBytes = 256 + (8 * 256 + 8) * sizeof(double);  // counter, CTA pairs, root ends
 inline int64_t plan_blocks_dev(int64_t n, int64_t m) {  // make_plan's block count, partition.hpp:30-49
     if (m >= n) return 1;
     int64_t leading = n / m;
@@ -142,7 +142,8 @@ inline int64_t plan_blocks_dev(int64_t n, int64_t m) {  // make_plan's block cou
 bool grid_fits(int64_t n, int64_t m, size_t elem, int sms);
 template <class T>
 cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x, void* scratch,
-                              unsigned long long* err, int level, int sms, cudaStream_t st);
+                              unsigned long long* err, int level, int sms, cudaStream_t st, int mode = kSolve,
+                              const ShardLink* link = nullptr);
 template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st);

@@ -93,10 +93,14 @@ print(json.dumps({"m": out, "same": bool(np.array_equal(xs[0], xs[1]) and np.arr
 @pytest.mark.parametrize("n,P", [(40_000_000, 8), (12_800_000, 2), (8_000_000, 1)])
 def test_fused_shard_runs_the_single_gpu_graph(tp, n, P):
     """Each rank of the fused multi-GPU solve runs the single-GPU graph on its
-    shard: granule-aligned shards (m0*m1/2 rows) keep levels 0-1 tail-free, so
-    Stage 1 of levels 0-2 is the folded kernel and the deepest level is the
-    fused cluster kernel with the peer exchange at its root — the same kernels,
-    in the same order, as a single-GPU solve of a shard-sized system."""
+    shard, with the peer exchange at the root of its deepest kernel — the same
+    kernels, in the same order, as a single-GPU solve of a shard-sized system.
+    One rank per GPU (P = 1 here): Stage 1 of level 0, then the grid solve from
+    level 1 (k_grid_solve<kShard>) with the exchange at its root, Stage 3 of
+    level 0. Ranks sharing one GPU (P > 1 simulated here) keep the level path:
+    granule-aligned shards (m0*m1/2 rows) keep levels 0-1 tail-free, so Stage
+    1 of levels 0-2 is the folded kernel and the deepest level is the fused
+    cluster kernel with the exchange at its root."""
     m = _run_sim(_METRICS + f"""
 n, P = {n}, {P}
 pol = [64, 10, 32, 16]
@@ -106,19 +110,24 @@ ks = []
 x = sharded.simulate_ranks_fused(s.sub, s.diag, s.sup, s.rhs, P, pol, kernels=ks)
 g = sharded.shard_granule(pol)
 single = []
-tp.context().set_grid(False)  # the level path: the sharded graph has no grid solve
+tp.context().set_grid(P == 1)  # ranks sharing a GPU take the level path
 for r in range(P):
     lo, cnt = sharded.shard_bounds(n, P, r, g)
     sysr = tp.TridiagonalSystem(*(a[lo:lo + cnt].copy() for a in (s.sub, s.diag, s.sup, s.rhs)))
     tp.solve_partition(sysr, tp.RecursionPolicy(pol))
     single.append(tp.context().last_kernels())
+tp.context().set_grid(True)
 print(json.dumps({{"m": metrics(s, x, ref), "ks": ks, "single": single}}))
 """)
     assert _ok(m["m"]), m["m"]
     for ks, single in zip(m["ks"], m["single"]):
-        assert ks[0] == "stage1_fold2:L0", ks
-        assert "level_exchange:L3" in ks, ks
-        assert [k.replace("level_exchange", "level_final") for k in ks] == single, (ks, single)
+        if P == 1:
+            assert ks == ["stage1:L0", "grid_exchange:L1", "stage3:L0"], ks
+        else:
+            assert ks[0] == "stage1_fold2:L0", ks
+            assert "level_exchange:L3" in ks, ks
+        assert [k.replace("level_exchange", "level_final").replace("grid_exchange", "grid_solve") for k in ks] \
+            == single, (ks, single)
 
 
 @needs_shared_gpu
