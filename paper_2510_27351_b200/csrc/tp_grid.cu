@@ -306,7 +306,15 @@ constexpr int kGridChunksPerThread = 2;
 // grid-barrier spin bound (>= 32 ns each): ~0.5-1 s before the solve reports an error
 constexpr long kGridSpins = 1L << 24;
 // phase timestamps (%globaltimer) of every CTA when a launch asks for them
-__device__ unsigned long long g_grid_trace[2 * 256 * 8];  // [0, 2048) %globaltimer, then clock64
+constexpr int kGridTraceSlots = 16;  // per CTA
+__device__ unsigned long long g_grid_trace[2 * 256 * kGridTraceSlots];  // [0, 4096) %globaltimer, then clock64
+#define TP_GRID_STAMP(k)                                                                           \
+    do {                                                                                           \
+        if (tr) {                                                                                  \
+            g_grid_trace[kGridTraceSlots * b + (k)] = global_ns();                                 \
+            g_grid_trace[256 * kGridTraceSlots + kGridTraceSlots * b + (k)] = clock64();           \
+        }                                                                                          \
+    } while (0)
 
 // Block range of CTA b: blocks [K*b/P, K*(b+1)/P) of make_plan(n, m).
 struct GridGeom {
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     const bool tr = geo.trace != 0 && tid == 0;
     bool flag = false;  // a pivot below kPivotFloor (reported with this thread's first row)
     pdl_begin();
-    if (tr) { g_grid_trace[8 * b + 0] = global_ns(); g_grid_trace[2048 + 8 * b + 0] = clock64(); }
+    TP_GRID_STAMP(0);
 
     // ---- this CTA's rows: whole blocks [kb0, kb1) ----
     const int64_t kb0 = K * b / P, kb1 = K * (b + 1) / P;
@@ -391,7 +399,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    if (tr) { g_grid_trace[8 * b + 1] = global_ns(); g_grid_trace[2048 + 8 * b + 1] = clock64(); }
+    TP_GRID_STAMP(1);
 
     // ---- chunk geometry (block-aligned: a full block is 2^lg chunks) ----
     const int lo = mm >> lg, ex = mm & (g - 1);
@@ -428,7 +436,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         }
         cur = lb > 0 ? merge_schur(EA, EB, flag, s0) : EA;
     }
-    if (tr) { g_grid_trace[8 * b + 2] = global_ns(); g_grid_trace[2048 + 8 * b + 2] = clock64(); }
+    TP_GRID_STAMP(2);
 
     // ---- thread tree: 5 shuffle levels per warp ----
     SchurSave<T> sw[5];
@@ -439,6 +447,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         if ((lane & (2 * h - 1)) == 0 && tid + h < NTh) cur = merge_schur(cur, oth, flag, sw[lv]);
     }
     const int nwr = (NTh + 31) / 32;
+    TP_GRID_STAMP(8);
     if (lane == 0 && warp < nwr) wroot[warp] = cur;
     if (tid < 8) tside[tid] = 0;
     __syncthreads();
@@ -461,7 +470,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             T* o = pairs + 8 * (int64_t)b;
             o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
             o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
-            if (tr) { g_grid_trace[8 * b + 3] = global_ns(); g_grid_trace[2048 + 8 * b + 3] = clock64(); }
+            TP_GRID_STAMP(3);
             __threadfence();
             atomicAdd(bar, 1u);  // arrive; the wait comes after the symbolic pass
         }
@@ -511,7 +520,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             }
         }
     }
-    if (tr) { g_grid_trace[8 * b + 4] = global_ns(); g_grid_trace[2048 + 8 * b + 4] = clock64(); }
+    TP_GRID_STAMP(4);
 
     // ---- the grid barrier: every CTA's pair is published ----
     if (tid == 0) {
@@ -525,6 +534,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             __nanosleep(32);
         }
     }
+    TP_GRID_STAMP(9);
     __syncthreads();
 
     // ---- every CTA: the tree over the P CTA pairs (identical arithmetic in
@@ -539,6 +549,8 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 tc = Eq2<T>{__ldcg(q + 0), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3),
                             __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
             }
+            if (tr) { volatile T sink = tc.d2; (void)sink; }
+            TP_GRID_STAMP(10);
 #pragma unroll
             for (int lv = 0; lv < 5; ++lv) {
                 const int h = 1 << lv;
@@ -553,6 +565,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 }
             }
             if (lane == 0) troot[warp] = tc;
+            TP_GRID_STAMP(11);
         }
         __syncthreads();
         if (warp == 0) {
@@ -572,6 +585,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 }
             }
             __syncwarp();
+            TP_GRID_STAMP(12);
             if (lane == 0) {
                 // root (thomas_solve on [E1; E2]), then down the path to leaf b
                 T xs = 0, xe = 0;
@@ -619,11 +633,12 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 }
                 cx[0] = xs;
                 cx[1] = xe;
+                TP_GRID_STAMP(13);
             }
         }
         __syncthreads();
     }
-    if (tr) { g_grid_trace[8 * b + 5] = global_ns(); g_grid_trace[2048 + 8 * b + 5] = clock64(); }
+    TP_GRID_STAMP(5);
 
     // ---- every warp: its root's ends W0, W1, then x = c + u W0 + v W1 over
     //      its rows (lane-strided, coalesced) ----
@@ -643,11 +658,11 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             nf |= !isfinite(v);
         }
     }
-    if (tr) { g_grid_trace[8 * b + 6] = global_ns(); g_grid_trace[2048 + 8 * b + 6] = clock64(); }
+    TP_GRID_STAMP(6);
     if (nf) report_nonfinite(err, r0);
     if (flag) report_pivot(err, level, r0 + la0);
     if (tflag) report_pivot(err, level, r0);
-    if (tr) { g_grid_trace[8 * b + 7] = global_ns(); g_grid_trace[2048 + 8 * b + 7] = clock64(); }
+    TP_GRID_STAMP(7);
 }
 
 // ---------------------------------------------------------------- host side
@@ -745,6 +760,6 @@ template cudaError_t launch_grid_solve<float>(const SysPtrs<float>&, int64_t, in
 
 // Phase timestamps of the last traced launch (TPB_GRID_TRACE=1): 8 per CTA.
 extern "C" int tp_debug_grid_trace(unsigned long long* out, int count) {
-    if (count > 2 * 256 * 8) count = 2 * 256 * 8;
+    if (count > 2 * 256 * tpb::kGridTraceSlots) count = 2 * 256 * tpb::kGridTraceSlots;
     return (int)cudaMemcpyFromSymbol(out, tpb::g_grid_trace, (size_t)count * sizeof(unsigned long long));
 }

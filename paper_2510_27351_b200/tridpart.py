@@ -683,7 +683,7 @@ def default_depth_model() -> HeuristicModel:
 
 def b200_size_model() -> HeuristicModel:
     """The m-predictor re-fitted on the B200 (config 5): fit_knn(k=1) of the
-    plateau-corrected sweep_m observations in profiles/r01_sweep_b200.csv
+    plateau-corrected sweep_m observations in profiles/r02_sweep_b200.csv
     (heuristics/b200_fp64_size_model.json). Device-specific, as the paper
     expects; the reference-parity default stays
     default_size_model()."""

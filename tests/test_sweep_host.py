@@ -61,12 +61,12 @@ def test_plateau_single_run_and_missing_times(tp):
 
 def test_bundled_b200_size_model_is_the_refit_of_the_committed_sweep(tp):
     """heuristics/b200_fp64_size_model.json = fit_knn(k=1) of the plateau-
-    corrected B200 sweep (profiles/r01_sweep_b200.csv, config 5): same pairs,
+    corrected B200 sweep (profiles/r02_sweep_b200.csv, config 5): same pairs,
     same predictions; the reference-parity default model is unchanged."""
     import os
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    obs = tp.read_observations(os.path.join(root, "profiles", "r01_sweep_b200.csv"))
+    obs = tp.read_observations(os.path.join(root, "profiles", "r02_sweep_b200.csv"))
     refit = tp.fit_knn(obs.with_corrected_labels(), 1)
     bundled = tp.b200_size_model()
     assert [(p.n, p.label) for p in bundled.pairs] == [(p.n, p.label) for p in refit.pairs]
@@ -74,4 +74,5 @@ def test_bundled_b200_size_model_is_the_refit_of_the_committed_sweep(tp):
     for n in (100, 4_500, 60_000, 1_000_000, 100_000_000, 1_000_000_000):
         assert tp.predict(bundled, n) == tp.predict(refit, n)
     assert tp.predicted_policy(100_000_000).sizes == [64, 10, 32, 16]  # reference models
-    assert tp.predicted_policy(100_000_000, size_model=bundled).sizes[0] == 64
+    # on the round-2 kernels the plateau-corrected B200 optimum at 1e8 is m = 128
+    assert tp.predicted_policy(100_000_000, size_model=bundled).sizes[0] == 128

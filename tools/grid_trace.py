@@ -12,7 +12,11 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-PHASES = ["start", "staged", "leaves", "pair", "barrier", "top", "expanded", "stored"]
+SLOTS = 16
+# slot -> phase name, in time order
+PHASES = [(0, "start"), (1, "staged"), (2, "leaves"), (8, "thread tree"), (3, "pair published"),
+          (4, "symbolic done"), (9, "barrier passed"), (10, "pairs loaded"), (11, "top warp tree"),
+          (12, "top root tree"), (13, "root + path"), (5, "top synced"), (6, "x stored"), (7, "end")]
 
 
 def main():
@@ -37,9 +41,9 @@ def main():
         tp.solve_partition_async(sys_, pol, out=x)
     torch.cuda.synchronize()
     assert tp.context().last_kernels() == ["grid_solve:L0"], tp.context().last_kernels()
-    buf = (C.c_ulonglong * (2 * 256 * 8))()
-    lib.tp_debug_grid_trace(buf, 2 * 256 * 8)
-    allv = np.array(buf[:], dtype=np.int64).reshape(2, 256, 8)
+    buf = (C.c_ulonglong * (2 * 256 * SLOTS))()
+    lib.tp_debug_grid_trace(buf, 2 * 256 * SLOTS)
+    allv = np.array(buf[:], dtype=np.int64).reshape(2, 256, SLOTS)
     live = allv[0, :, 0] > 0
     t = allv[0][live]
     clk = allv[1][live]
@@ -50,7 +54,7 @@ def main():
     t0 = t[:, 0].min()
     d = (t - t0) / 1000.0
     rows = {}
-    for k, ph in enumerate(PHASES):
+    for k, ph in PHASES:
         rows[ph] = [round(float(np.min(d[:, k])), 3), round(float(np.median(d[:, k])), 3),
                     round(float(np.max(d[:, k])), 3)]
         print(f"{ph:>9}  min {rows[ph][0]:8.3f}  med {rows[ph][1]:8.3f}  max {rows[ph][2]:8.3f} us"
