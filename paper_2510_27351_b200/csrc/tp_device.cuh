@@ -344,24 +344,6 @@ __device__ __forceinline__ Eq2<T> merge_schur(const Eq2<T>& A, const Eq2<T>& B, 
     P.d2 = fma(-B.a2, sv.ud, B.d2);
     return P;
 }
-// Stage-1-only form (no saves): every output row is one FMA after rcp(det).
-template <class T>
-__device__ __forceinline__ Eq2<T> merge_schur_up(const Eq2<T>& A, const Eq2<T>& B, bool& flag) {
-    const T det = fma(A.b2, B.b1, -(A.g2 * B.a1));
-    const T r = rcp(det);
-    const T fl = pivot_floor<T>();
-    flag |= (fabs(B.b1) < fl) | (fabs(A.b2) < fl) | (fabs(det) < fl * fabs(B.b1)) | (fabs(det) < fl * fabs(A.b2));
-    Eq2<T> P;
-    P.a1 = A.a1;
-    P.b1 = fma(-(A.g1 * B.b1 * A.a2), r, A.b1);
-    P.g1 = (A.g1 * A.g2 * B.g1) * r;
-    P.d1 = fma(-A.g1 * fma(B.b1, A.d2, -(A.g2 * B.d1)), r, A.d1);
-    P.a2 = (B.a2 * B.a1 * A.a2) * r;
-    P.b2 = fma(-(B.a2 * A.b2 * B.g1), r, B.b2);
-    P.g2 = B.g2;
-    P.d2 = fma(-B.a2 * fma(A.b2, B.d1, -(B.a1 * A.d2)), r, B.d2);
-    return P;
-}
 template <class T>
 __device__ __forceinline__ void schur_down(const SchurSave<T>& sv, T xs, T xe, T& xt, T& xt1) {
     xt = fma(sv.sg, xe, fma(-sv.sa, xs, sv.sd));

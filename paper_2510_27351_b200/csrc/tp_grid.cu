@@ -326,22 +326,6 @@ struct GridGeom {
     int trace;
 };
 
-// One step down a Schur merge node held by `left` lanes (h apart): the left
-// child keeps (xs, x_t), the right child gets (x_{t+1}, xe).
-template <class T>
-__device__ __forceinline__ void schur_step(const SchurSave<T>& sv, bool left, bool right, int h, T& xs, T& xe) {
-    T xt = 0, xt1 = 0;
-    if (left) schur_down(sv, xs, xe, xt, xt1);
-    const T rx1 = __shfl_up_sync(0xffffffffu, xt1, h);
-    const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
-    if (right) {
-        xs = rx1;
-        xe = rxe;
-    } else if (left) {
-        xe = xt;
-    }
-}
-
 // MODE kSolve: the root pair is the whole system (thomas_solve on [E1; E2]).
 // MODE kShard: the root pair is this rank's shard; CTA 0 exchanges it with
 // every peer over peer memory (shard_exchange, tp_exchange.cuh), solves the
