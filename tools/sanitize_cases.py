@@ -81,6 +81,12 @@ def main():
     # to and waits on its own mailbox, so no second kernel has to run alongside
     xf = sharded.simulate_ranks_fused(s.sub, s.diag, s.sup, s.rhs, 1, [16])
     assert oracle.rel_inf_diff(xf, ref) <= 1e-10
+    # the same with the grid solve at the root (k_grid_solve<double, L, kShard>):
+    # one rank owns the GPU, the shard's system fits the grid
+    s = oracle.generate_system(200_000, 13)
+    ref = oracle.solve_partition(s, [32])
+    xg = sharded.simulate_ranks_fused(s.sub, s.diag, s.sup, s.rhs, 1, [32])
+    assert oracle.rel_inf_diff(xg, ref) <= 1e-10
     torch.cuda.synchronize()
     print(f"sanitize cases ok (worst rel_inf_diff {worst:.2e})")
 
