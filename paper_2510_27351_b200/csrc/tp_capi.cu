@@ -416,11 +416,24 @@ struct Runner {
     // Whole solve: reset the error word, Stage 1 down, finish, Stage 3 up —
     // or, for a one-level policy that fits the grid's shared memory, the one
     // co-resident kernel k_grid_solve (tp_grid.cu).
+    // When the whole solve is one kernel (the grid solve from level 0, or the
+    // fused deepest level of a one-level plan) that kernel resets the error
+    // word itself and the graph has no k_reset node.
+    bool single_kernel(const Plan<T>& p, int mode) const {
+        const int gk = grid_level_for(p, mode);
+        if (gk >= 0) return gk == 0;
+        const size_t nl = p.levels.size();
+        return nl == 1 && !p.levels[0].split &&
+               tpb::level_final_fits(p.levels[0].n, p.levels[0].m, p.levels[0].K, sizeof(T), p.cs);
+    }
     void solve(const Plan<T>& p) {
-        const bool grid = grid_level(ctx, p) >= 0;
-        check(tpb::launch_reset(ctx->d_err, st, grid ? static_cast<unsigned*>(ctx->d_grid) : nullptr));
+        if (single_kernel(p, tpb::kSolve)) {
+            solve_body(p, tpb::kSolve, tpb::kResetErr);
+            return;
+        }
+        check(tpb::launch_reset(ctx->d_err, st));
         ++launches;  // k_reset: counted, not timed by the profile hook
-        solve_body(p, tpb::kSolve, grid);
+        solve_body(p, tpb::kSolve);
     }
     // Stage 1 of levels [0, top): level 1's (and level 2's) folded into level
     // 0's kernel (k_fast_s1fold) where the shapes allow, the rest per level.
@@ -450,14 +463,14 @@ struct Runner {
     // mode kShard (sharded plan, fused = true): the same graph with the peer
     // exchange at the root of the deepest level (k_level_final_cl<kShard>) or
     // of the finishing solve (k_final<kShard>).
-    void solve_body(const Plan<T>& p, int mode = tpb::kSolve, bool bar_zeroed = false) {
+    // flags = kResetErr: the plan is one kernel, which resets the error word.
+    void solve_body(const Plan<T>& p, int mode = tpb::kSolve, int flags = 0) {
         const int gk = grid_level_for(p, mode);
         if (gk >= 0) {  // Stage 1 down to level gk, the grid solve from there, Stage 3 up
             stage1_down(p, (size_t)gk);
             const Level<T>& G = p.levels[(size_t)gk];
-            if (!bar_zeroed) check(cudaMemsetAsync(ctx->d_grid, 0, sizeof(unsigned), st));
             check(tpb::launch_grid_solve<T>(G.in, G.n, G.m, G.x_out, ctx->d_grid, ctx->d_err, gk, ctx->sms, st, mode,
-                                            mode == tpb::kShard ? &ctx->link : nullptr));
+                                            mode == tpb::kShard ? &ctx->link : nullptr, flags));
             after(mode == tpb::kShard ? "grid_exchange" : "grid_solve", gk);
             for (int l = gk; l-- > 0;) stage(p.levels[(size_t)l], l, tpb::kStage3);
             return;
@@ -471,7 +484,7 @@ struct Runner {
         if (fuse) {
             const Level<T>& L = p.levels.back();
             check(tpb::launch_level_final<T>(L.in, L.n, L.m, L.K, L.iface, L.x_out, ctx->d_err, (int)top, st, mode,
-                                             mode == tpb::kShard ? &ctx->link : nullptr, p.cs));
+                                             mode == tpb::kShard ? &ctx->link : nullptr, p.cs, top == 0 ? flags : 0));
             after(mode == tpb::kShard ? "level_exchange" : "level_final", (int)top);
         } else if (mode == tpb::kShard) {
             check(tpb::launch_final<T>(tpb::kShard, p.final_in, p.n_final, IfacePtrs<T>{}, nullptr, p.final_x,
@@ -497,10 +510,13 @@ struct Runner {
     // the deepest level fused with the finishing solve, Stage 3 up) with the
     // peer exchange and the top solve at the root of the deepest level.
     void shard_solve(const Plan<T>& p) {
-        const bool grid = grid_level_for(p, tpb::kShard) >= 0;
-        check(tpb::launch_reset(ctx->d_err, st, grid ? static_cast<unsigned*>(ctx->d_grid) : nullptr));
+        if (single_kernel(p, tpb::kShard)) {
+            solve_body(p, tpb::kShard, tpb::kResetErr);
+            return;
+        }
+        check(tpb::launch_reset(ctx->d_err, st));
         ++launches;  // k_reset: counted, not timed by the profile hook
-        solve_body(p, tpb::kShard, grid);
+        solve_body(p, tpb::kShard);
     }
     void shard_finish(const Plan<T>& p, const T* eq_all, int nranks, int rank) {
         T* x2 = static_cast<T*>(ctx->d_small);

@@ -572,7 +572,7 @@ __device__ __forceinline__ void lf_expand_regs(T* a, const T* rbp, const T* gp, 
 template <class T, int MF, int CS, int MODE>
 __global__ void __launch_bounds__(kFinNT, 1)
     k_level_final_cl(SysPtrs<T> sys, int64_t n, int m, int64_t K, int S, IfacePtrs<T> iface, T* __restrict__ x,
-                     unsigned long long* err, int level, const __grid_constant__ ShardLink link) {
+                     unsigned long long* err, int level, const __grid_constant__ ShardLink link, int flags) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char lf_raw[];
@@ -589,6 +589,10 @@ __global__ void __launch_bounds__(kFinNT, 1)
     RowGuard bad_lv, bad_fin;
     pdl_begin();
     TP_LF_TRACE(0);
+    if ((flags & kResetErr) && cta == 0 && tid == 0 && err != nullptr) {  // the graph's only kernel
+        atomicExch(err, kNoError);
+        __threadfence();
+    }
 
     const int64_t r0 = B0 * m;
     const int rows = (int)((B1 == K ? n : B1 * m) - r0);

@@ -324,7 +324,19 @@ struct GridGeom {
     int S;   // smem stride of one array, in elements (padded)
     int qs;  // pad shift (one pad element per 2^qs rows)
     int trace;
+    int flags;  // kResetErr: the graph's only kernel resets the error word
 };
+
+// The grid barrier's counters: bar[0] counts arrivals (P, then P + 1 when
+// the sharded root ends are out), bar[1] departures. The last CTA to leave
+// resets both, so every launch starts from zero without a reset node.
+__device__ __forceinline__ void grid_depart(unsigned* bar, int P) {
+    if (atomicAdd(bar + 1, 1u) == (unsigned)P - 1u) {
+        bar[0] = 0u;
+        bar[1] = 0u;
+        __threadfence();
+    }
+}
 
 // MODE kSolve: the root pair is the whole system (thomas_solve on [E1; E2]).
 // MODE kShard: the root pair is this rank's shard; CTA 0 exchanges it with
@@ -455,6 +467,9 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
             o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
             TP_GRID_STAMP(3);
+            // the graph's only kernel: reset the error word before arriving
+            // (every report of this solve comes after the barrier)
+            if ((geo.flags & kResetErr) && b == 0 && err != nullptr) atomicExch(err, kNoError);
             __threadfence();
             atomicAdd(bar, 1u);  // arrive; the wait comes after the symbolic pass
         }
@@ -519,6 +534,9 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         }
     }
     TP_GRID_STAMP(9);
+    if constexpr (MODE != kShard) {
+        if (tid == 0) grid_depart(bar, P);
+    }
     __syncthreads();
 
     // ---- every CTA: the tree over the P CTA pairs (identical arithmetic in
@@ -599,6 +617,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                         xs = __ldcg(root);
                         xe = __ldcg(root + 1);
                     }
+                    grid_depart(bar, P);
                 } else {
                     RowGuard rg;
                     root_solve(rc, n - 1, rg, xs, xe);
@@ -675,7 +694,7 @@ static bool grid_geom(int64_t n, int64_t m, int sms, GridGeom& geo) {
     const int64_t S = ((rows + (rows >> qs) + 1 + 3) / 4) * 4;
     if (grid_smem_bytes(S, sizeof(T)) > kGridDynSmem) return false;
     static const int trace = [] { const char* v = getenv("TPB_GRID_TRACE"); return v ? atoi(v) : 0; }();
-    geo = GridGeom{n, m, K, lg, P, (int)S, qs, trace};
+    geo = GridGeom{n, m, K, lg, P, (int)S, qs, trace, 0};
     return true;
 }
 
@@ -696,9 +715,10 @@ static GridKernel<T, MODE> grid_kernel(int L) {
 template <class T>
 cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x, void* scratch,
                               unsigned long long* err, int level, int sms, cudaStream_t st, int mode,
-                              const ShardLink* link) {
+                              const ShardLink* link, int flags) {
     GridGeom geo;
     if (!grid_geom<T>(n, m, sms, geo)) return cudaErrorInvalidValue;
+    geo.flags = flags;
     if (mode == kShard && (sizeof(T) != 8 || link == nullptr || link->nranks < 1 || link->nranks > kMaxPeers))
         return cudaErrorInvalidValue;  // the mailboxes carry FP64 pairs
     unsigned* bar = static_cast<unsigned*>(scratch);
@@ -736,9 +756,11 @@ cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x,
 }
 
 template cudaError_t launch_grid_solve<double>(const SysPtrs<double>&, int64_t, int64_t, double*, void*,
-                                               unsigned long long*, int, int, cudaStream_t, int, const ShardLink*);
+                                               unsigned long long*, int, int, cudaStream_t, int, const ShardLink*,
+                                               int);
 template cudaError_t launch_grid_solve<float>(const SysPtrs<float>&, int64_t, int64_t, float*, void*,
-                                              unsigned long long*, int, int, cudaStream_t, int, const ShardLink*);
+                                              unsigned long long*, int, int, cudaStream_t, int, const ShardLink*,
+                                              int);
 
 }  // namespace tpb
 

@@ -160,17 +160,13 @@ static cudaError_t launch_k(int level, void (*kern)(KArgs...), unsigned grid, un
 
 // Error-word reset at the head of every solve (a kernel rather than a memset
 // node, so the first Stage-1 grid can be launched programmatically after it).
-// With `bar`, also zeroes the grid-barrier counter of k_grid_solve.
-__global__ void k_reset(unsigned long long* err, unsigned* bar) {
+__global__ void k_reset(unsigned long long* err) {
     pdl_begin();
-    if (threadIdx.x == 0) {
-        *err = kNoError;
-        if (bar != nullptr) *bar = 0u;
-    }
+    if (threadIdx.x == 0) *err = kNoError;
 }
 
-cudaError_t launch_reset(unsigned long long* err, cudaStream_t st, unsigned* bar) {
-    return launch_k(0, k_reset, 1, 32, 0, st, err, bar);
+cudaError_t launch_reset(unsigned long long* err, cudaStream_t st) {
+    return launch_k(0, k_reset, 1, 32, 0, st, err);
 }
 
 // Launch shapes chosen by measurement (tools/microbench/level_shapes.cu and
@@ -417,7 +413,7 @@ bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem, int cs) {
 
 template <class T>
 using LfKernel = void (*)(SysPtrs<T>, int64_t, int, int64_t, int, IfacePtrs<T>, T*, unsigned long long*, int,
-                          ShardLink);
+                          ShardLink, int);
 
 // kShard variants exist for FP64 only (the sharded C-ABI is FP64)
 template <class T, int CS, int MODE>
@@ -434,7 +430,7 @@ static LfKernel<T> level_final_kernel(int64_t m) {
 template <class T>
 cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, const IfacePtrs<T>& iface,
                                T* x, unsigned long long* err, int level, cudaStream_t st, int mode,
-                               const ShardLink* link, int cs) {
+                               const ShardLink* link, int cs, int flags) {
     if (!level_final_fits(n, m, K, sizeof(T), cs)) return cudaErrorInvalidValue;
     const int c = lf_cluster(cs);
     LfKernel<T> k = nullptr;
@@ -447,7 +443,7 @@ cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int6
     if (k == nullptr) return cudaErrorInvalidValue;
     const ShardLink none{};
     return launch_kc(level, (unsigned)c, k, (unsigned)c, kFinNT, level_final_smem(m, K, sizeof(T), c), st, sys, n,
-                     (int)m, K, level_final_stride(m), iface, x, err, level, link != nullptr ? *link : none);
+                     (int)m, K, level_final_stride(m), iface, x, err, level, link != nullptr ? *link : none, flags);
 }
 
 template <class T, int CS, int MODE>
@@ -603,7 +599,7 @@ cudaError_t launch_residual(const SysPtrs<T>& sys, int64_t n, const T* x, unsign
                                         unsigned long long*, int, cudaStream_t);                        \
     template cudaError_t launch_level_final<T>(const SysPtrs<T>&, int64_t, int64_t, int64_t,        \
                                                const IfacePtrs<T>&, T*, unsigned long long*, int,   \
-                                               cudaStream_t, int, const ShardLink*, int);           \
+                                               cudaStream_t, int, const ShardLink*, int, int);      \
     template cudaError_t launch_split<T>(int, const SysPtrs<T>&, int64_t, int64_t, int64_t, int64_t,   \
                                          int64_t, const IfacePtrs<T>&, const T*, T*,                \
                                          unsigned long long*, int, cudaStream_t);                   \

@@ -13,6 +13,10 @@ constexpr int kStage3 = 1;  // expand blocks from the next level's solution
 constexpr int kSolve = 2;   // whole system as one block: reduce, 2x2 root, expand
 constexpr int kShard = 3;   // one shard of a multi-GPU solve: reduce, exchange the boundary
                             // pair with every peer over peer memory, top solve, expand
+// Launch flag of a kernel that is a solve graph's only kernel: it resets the
+// error word itself (CTA 0, before the first cluster / grid barrier, which
+// every error report follows), so the graph needs no k_reset.
+constexpr int kResetErr = 1;
 
 constexpr int kFastThreads = 256;
 constexpr int kGenericThreads = 256;
@@ -65,7 +69,7 @@ struct ShardLink {
 inline size_t mailbox_bytes(int nranks) { return (size_t)2 * nranks * kMailboxEntryDoubles * sizeof(double); }
 
 cudaError_t init_kernel_attributes();
-cudaError_t launch_reset(unsigned long long* err, cudaStream_t st, unsigned* bar = nullptr);
+cudaError_t launch_reset(unsigned long long* err, cudaStream_t st);
 bool fast_shape(int64_t m, int* L, int* G);
 int fast_rt_G(int64_t m);
 
@@ -106,7 +110,7 @@ bool level_final_fits(int64_t n, int64_t m, int64_t K, size_t elem, int cs = 0);
 template <class T>
 cudaError_t launch_level_final(const SysPtrs<T>& sys, int64_t n, int64_t m, int64_t K, const IfacePtrs<T>& iface,
                                T* x, unsigned long long* err, int level, cudaStream_t st, int mode = kSolve,
-                               const ShardLink* link = nullptr, int cs = 0);
+                               const ShardLink* link = nullptr, int cs = 0, int flags = 0);
 // One split level (tp_split.cuh): nblocks blocks of blen rows starting at
 // row_base, nsub chunks each, chunk pairs written from pair q_base on.
 template <class T>
@@ -126,8 +130,8 @@ cudaError_t launch_ref_thomas(const SysPtrs<T>& sys, int64_t n, int64_t* out, cu
 // Whole-system solve on one co-resident grid (k_grid_solve, tp_grid.cu): a
 // one-level policy whose rows fit the GPU's aggregate shared memory, one CTA
 // per SM, one grid barrier. grid_fits says whether (n, m) fits; the launcher
-// returns cudaErrorInvalidValue when it does not. scratch: kGridScratchBytes of device memory whose first
-// word must be zeroed before every launch (k_reset does it).
+// returns cudaErrorInvalidValue when it does not. scratch: kGridScratchBytes of device memory, zeroed once
+// (the barrier counters reset themselves at the end of every launch).
 constexpr int kGridBarrierLevel = 0x7FFD;  // err-word level of a grid-barrier timeout
 constexpr int64_t kGridMaxChunk = 64;  // longest leaf chunk (rows)
 constexpr int64_t kGridMinRows = 4;
@@ -143,7 +147,7 @@ bool grid_fits(int64_t n, int64_t m, size_t elem, int sms);
 template <class T>
 cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x, void* scratch,
                               unsigned long long* err, int level, int sms, cudaStream_t st, int mode = kSolve,
-                              const ShardLink* link = nullptr);
+                              const ShardLink* link = nullptr, int flags = 0);
 template <class T>
 cudaError_t launch_gather_solve(const T* eqs, int nranks, int rank, T* x2, T* scratch,
                                 unsigned long long* err, int level, cudaStream_t st);

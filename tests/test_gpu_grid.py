@@ -52,7 +52,7 @@ def test_config2_runs_as_one_grid_kernel(tp, oracle_mod):
     ref = oracle_mod.solve_partition(s, pol.sizes, impl=_impl(oracle_mod))
     x = tp.solve_partition(_sys(tp, s), pol)
     assert tp.context().last_kernels() == ["grid_solve:L0"]
-    assert tp.context().last_launch_count() == 2  # k_reset + the grid kernel
+    assert tp.context().last_launch_count() == 1  # the grid kernel alone (it resets the error word)
     _check(oracle_mod, s, x, ref)
 
 

@@ -54,16 +54,12 @@ def main():
                 kind = "kernel"
             evs.append((e.time_range.start, e.time_range.end, nm, kind))
     evs.sort()
-    # split into replays: every solve graph starts with k_reset (fall back to
-    # gaps > 50 us for graphs without it)
-    groups, cur = [], []
-    for ev in evs:
-        if cur and ("k_reset" in ev[2] or ev[0] - max(c[1] for c in cur) > 50):
-            groups.append(cur)
-            cur = []
-        cur.append(ev)
-    if cur:
-        groups.append(cur)
+    # split into replays of the solve graph: it launches
+    # tp.context().last_launch_count() kernels (k_reset included when present;
+    # a one-kernel graph resets the error word itself)
+    per = max(1, tp.context().last_launch_count())
+    kern = [ev for ev in evs if ev[3] == "kernel"]
+    groups = [kern[i:i + per] for i in range(0, len(kern) - per + 1, per)]
     g = groups[-1]
     t0 = g[0][0]
     end_prev = t0
