@@ -708,7 +708,7 @@ using GridKernel = void (*)(SysPtrs<T>, GridGeom, T*, T*, unsigned*, unsigned lo
 
 template <class T, int MODE>
 static GridKernel<T, MODE> grid_kernel(int L) {
-    return L == 8 ? k_grid_solve<T, 8, MODE> : L == 4 ? k_grid_solve<T, 4, MODE>
+    return L == 8 ? k_grid_solve<T, 8, MODE> : L == 5 ? k_grid_solve<T, 5, MODE> : L == 4 ? k_grid_solve<T, 4, MODE>
            : L == 2 ? k_grid_solve<T, 2, MODE> : k_grid_solve<T, 0, MODE>;
 }
 
@@ -724,12 +724,13 @@ cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x,
     unsigned* bar = static_cast<unsigned*>(scratch);
     T* pairs = reinterpret_cast<T*>(static_cast<unsigned char*>(scratch) + 256);
     // chunk length as a compile-time constant when every full block splits
-    // into equal chunks of 2, 4 or 8 rows (unrolled register sweeps)
+    // into equal chunks of 2, 4, 5 or 8 rows (unrolled register sweeps; 5:
+    // the m = 10 / 20 / 40 levels of the kNN policies)
     const int64_t cl = geo.m >> geo.lg;
-    const int L = ((cl << geo.lg) == geo.m && (cl == 2 || cl == 4 || cl == 8)) ? (int)cl : 0;
+    const int L = ((cl << geo.lg) == geo.m && (cl == 2 || cl == 4 || cl == 5 || cl == 8)) ? (int)cl : 0;
     static bool attr_done[2] = {false, false};
     if (!attr_done[sizeof(T) == 8]) {
-        for (int l : {8, 4, 2, 0}) {
+        for (int l : {8, 5, 4, 2, 0}) {
             cudaError_t e = cudaFuncSetAttribute(grid_kernel<T, kSolve>(l), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)kGridDynSmem);
             if (e == cudaSuccess)
