@@ -174,6 +174,18 @@ def test_grid_observer_still_sees_the_interface(tp, oracle_mod):
     assert tp.context().last_kernels() == ["grid_solve:L0"]
 
 
+@pytest.mark.parametrize("n,m", [(100_000, 32), (400_000, 32), (600_001, 32), (262_144, 64), (50_000, 8),
+                                 (100_003, 16), (300_000, 4)])
+def test_grid_register_variant(tp, oracle_mod, n, m):
+    """k_grid_reg (rows in registers, re-read for Stage 3; L = 4 / 8 chunks, <= 5K
+    rows per SM) against the reference, tails included."""
+    s = oracle_mod.generate_system(n, 17 + n % 7)
+    ref = oracle_mod.solve_partition(s, [m], impl="port")
+    x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([m]))
+    assert tp.context().last_kernels() == ["grid_solve:L0"]
+    _check(oracle_mod, s, x, ref)
+
+
 def test_grid_matches_the_level_path(tp, oracle_mod):
     """TPB_GRID=0 (level kernels) and the grid kernel agree to rounding."""
     code = """
