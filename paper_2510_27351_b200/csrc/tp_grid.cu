@@ -1152,13 +1152,14 @@ cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x,
     cfg.numAttrs = 1;
     const ShardLink none{};
     const ShardLink& lk = (mode == kShard) ? *link : none;
-    // rows in registers (k_grid_reg) where that measured faster: 256-bit
-    // chunk loads (L = 4, 8) and <= ~5K rows per SM (its L2 re-read of the
-    // rows costs more than the shared-memory staging above that: 1e6 {32}
-    // 20.5 vs 20.0 us, 6e5 {32} 14.6 vs 15.6 us, 1e5 {32} 10.9 vs 11.8 us,
-    // C3's level 2 17.9 vs 18.4 us; tools/ab_grid_reg.sh)
+    // rows in registers (k_grid_reg) where that measured faster: chunks of
+    // 2, 4 or 8 rows (5-row chunks: 18.8 vs 15.8 us at 6e5 {20}) and <= ~5K
+    // rows per SM (its L2 re-read of the rows costs more than the shared-
+    // memory staging above that: 1e6 {32} 20.5 vs 20.0 us, 6e5 {32} 14.6 vs
+    // 15.6 us, 1e5 {32} 10.9 vs 11.8 us, C3's level 2 17.9 vs 18.4 us;
+    // tools/ab_grid_reg.sh)
     const int64_t rows_cta = ((geo.K + geo.P - 1) / geo.P) * geo.m;
-    if ((L == 8 || L == 4) && rows_cta <= 5000 && g_greg == 1) {
+    if ((L == 8 || L == 4 || L == 2) && rows_cta <= 5000 && g_greg == 1) {
         auto a32 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; };
         const int vec = a32(sys.sub) && a32(sys.diag) && a32(sys.sup) && a32(sys.rhs) && a32(x) ? 1 : 0;
         cfg.dynamicSmemBytes = greg_smem_bytes(sizeof(T));
