@@ -1046,6 +1046,369 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     if (tflag) report_pivot(err, level, r0);
 }
 
+// ===========================================================================
+// k_grid_hyb: rows loaded into registers (256-bit) and swept from there, as
+// k_grid_reg, but also copied into the padded shared-memory layout of
+// k_grid_solve, so Stage 3 reads them back from shared memory instead of L2;
+// the merge saves stay in registers (as k_grid_solve). Shared-memory traffic:
+// 8 values per row (k_grid_solve: 17), no L2 re-read (k_grid_reg).
+// ===========================================================================
+template <class T, int L, int MODE>
+__global__ void __launch_bounds__(kGridThreads, 1)
+    k_grid_hyb(SysPtrs<T> sys, GridGeom geo, T* __restrict__ x, T* pairs, unsigned* bar,
+               unsigned long long* err, int level, const __grid_constant__ ShardLink link, int vec) {
+    static_assert(L >= 2 && L <= 8, "register chunks of 2..8 rows");
+    extern __shared__ __align__(16) unsigned char ghyb_smem[];
+    T* sa = reinterpret_cast<T*>(ghyb_smem);  // the CTA's rows, padded (as k_grid_solve)
+    T* sb = sa + geo.S;
+    T* sc = sb + geo.S;
+    T* sd = sc + geo.S;
+    const int qs = geo.qs;
+    __shared__ Eq2<T> wroot[kGridWarps];
+    __shared__ SchurSave<T> wsv[kGridWarps - 1];
+    __shared__ Eq2<T> troot[8];
+    __shared__ SchurSave<T> tpath[8];
+    __shared__ int tside[8];
+    __shared__ T wx[2 * kGridWarps];
+    __shared__ T cx[2];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b = blockIdx.x, P = geo.P;
+    const int64_t n = geo.n, m = geo.m, K = geo.K;
+    const int lg = geo.lg;
+    const bool tr = geo.trace != 0 && tid == 0;
+    pdl_begin();
+    TP_GRID_STAMP(0);
+
+    // ---- this CTA's rows: whole blocks [kb0, kb1) (as k_grid_solve) ----
+    const int64_t kb0 = K * b / P, kb1 = K * (b + 1) / P;
+    const int64_t r0 = kb0 * m;
+    const int64_t r1 = (kb1 == K) ? n : kb1 * m;
+    const int R = (int)(r1 - r0);
+    const bool has_tail = (kb1 == K) && (n - (K - 1) * m != m);
+    const int nfull = (int)((kb1 - kb0) - (has_tail ? 1 : 0));
+    const int tlen = has_tail ? (int)(n - (K - 1) * m) : 0;
+    const int g = 1 << lg;
+    int lgt = 0;
+    if (has_tail)
+        while ((1 << (lgt + 1)) <= g && tlen >= 4 << lgt) ++lgt;
+    const int C = nfull * g + (has_tail ? 1 << lgt : 0);
+    const int NTh = (C + 1) / 2;
+    const int mm = (int)m;
+    const int tail0 = nfull * mm;  // CTA-local first row of the tail block
+    const int tlo = tlen >> lgt, tex = tlen & ((1 << lgt) - 1);
+    auto cstart = [&](int c) -> int {
+        if (c >= C) return R;
+        const int blk = c >> lg;
+        if (blk < nfull) return c * L;  // full blocks: uniform chunks of L rows
+        const int q = c - (nfull << lg);
+        return tail0 + q * tlo + (q < tex ? q : tex);
+    };
+    if (has_tail) {  // stage the tail block (<= m + 1 rows) for its chunks' shared-memory sweeps
+        for (int i = tid; i < tlen; i += kGridThreads) {
+            const int k = padx(tail0 + i, qs);
+            sa[k] = sys.sub[r0 + tail0 + i];
+            sb[k] = sys.diag[r0 + tail0 + i];
+            sc[k] = sys.sup[r0 + tail0 + i];
+            sd[k] = sys.rhs[r0 + tail0 + i];
+        }
+    }
+    if (tid < 8) tside[tid] = 0;
+    __syncthreads();
+    TP_GRID_STAMP(1);
+
+    const bool active = tid < NTh;
+    int la0 = 0, la = 2, lb0 = 0, lb = 0;
+    if (active) {
+        la0 = cstart(2 * tid);
+        lb0 = cstart(2 * tid + 1);
+        la = lb0 - la0;
+        lb = (2 * tid + 1 < C) ? cstart(2 * tid + 2) - lb0 : 0;
+    }
+
+    // ---- leaves in registers: two chunks per thread, then their merge ----
+    MinGuard<T> mg;
+    bool flag = false;
+    // full chunks: rows loaded into registers (256-bit), copied to shared
+    // memory for Stage 3, swept from the registers; tail chunks: swept from
+    // shared memory (kept values in place)
+    auto leaf = [&](int l0, int len) -> Eq2<T> {
+        if (l0 < tail0 || !has_tail) {
+            Chunk<T, L> r;
+            const int64_t row0 = r0 + l0;
+            if (vec) load_chunk<T, L, true>(sys, row0, true, r);
+            else load_chunk<T, L, false>(sys, row0, true, r);
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+                const int k = padx(l0 + i, qs);
+                sa[k] = r.a[i];
+                sb[k] = r.b[i];
+                sc[k] = r.c[i];
+                sd[k] = r.d[i];
+            }
+            return leaf_reduce<T, L, L>(r, row0, mg);
+        }
+        Eq2<T> e;
+        leaf_loop<T>(sa, sb, sc, sd, l0, len, qs, flag, e);
+        return e;
+    };
+    Eq2<T> cur = identity_eq<T>();
+    SchurSave<T> s0{};
+    if (active) {
+        const Eq2<T> EA = leaf(la0, la);
+        if (lb > 0) {
+            const Eq2<T> EB = leaf(lb0, lb);
+            cur = merge_schur(EA, EB, flag, s0);
+        } else {
+            cur = EA;
+        }
+    }
+    TP_GRID_STAMP(2);
+
+    // ---- thread tree (5 shuffle levels), saves in registers ----
+    SchurSave<T> sw[5];
+#pragma unroll
+    for (int lv = 0; lv < 5; ++lv) {
+        const int h = 1 << lv;
+        const Eq2<T> oth = shfl_down_eq(cur, h);
+        if ((lane & (2 * h - 1)) == 0 && tid + h < NTh) cur = merge_schur(cur, oth, flag, sw[lv]);
+    }
+    const int nwr = (NTh + 31) / 32;
+    TP_GRID_STAMP(8);
+    if (lane == 0 && warp < nwr) wroot[warp] = cur;
+    __syncthreads();
+
+    // ---- warp 0: the warp roots -> this CTA's pair, published ----
+    if (warp == 0) {
+        Eq2<T> wc = lane < nwr ? wroot[lane] : identity_eq<T>();
+#pragma unroll
+        for (int lv = 0, off = 0; lv < 4; off += kGridWarps >> (lv + 1), ++lv) {
+            const int h = 1 << lv;
+            const Eq2<T> oth = shfl_down_eq(wc, h);
+            if ((lane & (2 * h - 1)) == 0 && lane + h < nwr) {
+                SchurSave<T> sv;
+                wc = merge_schur(wc, oth, flag, sv);
+                wsv[off + (lane >> (lv + 1))] = sv;
+            }
+        }
+        if (lane == 0) {
+            T* o = pairs + 8 * (int64_t)b;
+            o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
+            o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
+            TP_GRID_STAMP(3);
+            if ((geo.flags & kResetErr) && b == 0 && err != nullptr) atomicExch(err, kNoError);
+            __threadfence();
+            atomicAdd(bar, 1u);
+            long spins = 0;
+            while (ld_acquire_gpu(bar) < (unsigned)P) {
+                if (++spins > kGridSpins) {
+                    if (err != nullptr)
+                        atomicMin(err, ((unsigned long long)kGridBarrierLevel << 48) | (unsigned long long)b);
+                    break;
+                }
+                __nanosleep(32);
+            }
+            if constexpr (MODE != kShard) grid_depart(bar, P);
+            TP_GRID_STAMP(9);
+        }
+    }
+    __syncthreads();
+
+    // ---- every CTA: the tree over the P CTA pairs, root, its own path (as k_grid_solve) ----
+    bool tflag = false;
+    {
+        const int ntw = (P + 31) / 32;
+        if (warp < ntw) {
+            Eq2<T> tc = identity_eq<T>();
+            if (tid < P) {
+                const T* q = pairs + 8 * (int64_t)tid;
+                tc = Eq2<T>{__ldcg(q + 0), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3),
+                            __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
+            }
+#pragma unroll
+            for (int lv = 0; lv < 5; ++lv) {
+                const int h = 1 << lv;
+                const Eq2<T> oth = shfl_down_eq(tc, h);
+                if ((lane & (2 * h - 1)) == 0 && tid + h < P) {
+                    SchurSave<T> sv;
+                    tc = merge_schur(tc, oth, tflag, sv);
+                    if ((tid >> (lv + 1)) == (b >> (lv + 1))) {
+                        tpath[3 + lv] = sv;
+                        tside[3 + lv] = ((b >> lv) & 1) ? 2 : 1;
+                    }
+                }
+            }
+            if (lane == 0) troot[warp] = tc;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            Eq2<T> rc = lane < ntw ? troot[lane] : identity_eq<T>();
+            const int bw = b >> 5;
+#pragma unroll
+            for (int lv = 0; lv < 3; ++lv) {
+                const int h = 1 << lv;
+                const Eq2<T> oth = shfl_down_eq(rc, h);
+                if ((lane & (2 * h - 1)) == 0 && lane + h < ntw) {
+                    SchurSave<T> sv;
+                    rc = merge_schur(rc, oth, tflag, sv);
+                    if ((lane >> (lv + 1)) == (bw >> (lv + 1))) {
+                        tpath[2 - lv] = sv;
+                        tside[2 - lv] = ((bw >> lv) & 1) ? 2 : 1;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                T xs = 0, xe = 0;
+                if constexpr (MODE == kShard) {
+                    T* root = pairs + 8 * 256;
+                    if (b == 0) {
+                        __shared__ double top_cm[2 * kMaxPeers], top_x[2 * kMaxPeers];
+                        RowGuard top_bad;
+                        int missing = -1;
+                        if (!shard_exchange(link, rc, top_cm, top_x, xs, xe, top_bad, missing) && err != nullptr)
+                            atomicMin(err, ((unsigned long long)kExchangeLevel << 48) | (unsigned long long)missing);
+                        report_pivot(err, level + 1, top_bad.bad);
+                        root[0] = xs;
+                        root[1] = xe;
+                        __threadfence();
+                        atomicAdd(bar, 1u);
+                    } else {
+                        long spins = 0;
+                        while (ld_acquire_gpu(bar) < (unsigned)P + 1u) {
+                            if (++spins > 2 * kExchangeSpins) {
+                                if (err != nullptr)
+                                    atomicMin(err, ((unsigned long long)kGridBarrierLevel << 48) | (unsigned long long)b);
+                                break;
+                            }
+                            __nanosleep(64);
+                        }
+                        xs = __ldcg(root);
+                        xe = __ldcg(root + 1);
+                    }
+                    grid_depart(bar, P);
+                } else {
+                    RowGuard rg;
+                    root_solve(rc, n - 1, rg, xs, xe);
+                    tflag |= rg.bad != INT64_MAX;
+                }
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k) {
+                    const int j = k < 3 ? k : 10 - k;  // warp-root levels 2, 1, 0, then warp levels 4..0
+                    if (tside[j] == 0) continue;
+                    T xt, xt1;
+                    schur_down(tpath[j], xs, xe, xt, xt1);
+                    if (tside[j] == 1) xe = xt;
+                    else xs = xt1;
+                }
+                cx[0] = xs;
+                cx[1] = xe;
+            }
+        }
+        __syncthreads();
+    }
+    TP_GRID_STAMP(5);
+
+    // ---- the CTA's tree top-down, numerically: warp roots, then every warp ----
+    if (warp == 0) {
+        T xs = lane == 0 ? cx[0] : T(0), xe = lane == 0 ? cx[1] : T(0);
+#pragma unroll
+        for (int lv = 3; lv >= 0; --lv) {
+            const int h = 1 << lv;
+            int off = 0;
+            for (int j = 0; j < lv; ++j) off += kGridWarps >> (j + 1);
+            const bool left = (lane & (2 * h - 1)) == 0 && lane + h < nwr;
+            const bool right = (lane & (2 * h - 1)) == h && lane < nwr;
+            T xt = 0, xt1 = 0;
+            if (left) schur_down(wsv[off + (lane >> (lv + 1))], xs, xe, xt, xt1);
+            const T r1 = __shfl_up_sync(0xffffffffu, xt1, h);
+            const T re = __shfl_up_sync(0xffffffffu, xe, h);
+            if (right) {
+                xs = r1;
+                xe = re;
+            } else if (left) {
+                xe = xt;
+            }
+        }
+        if (lane < nwr) {
+            wx[2 * lane] = xs;
+            wx[2 * lane + 1] = xe;
+        }
+    }
+    __syncthreads();
+    bool nf = false;
+    {
+        T xs = 0, xe = 0;
+        if (lane == 0 && warp < nwr) {
+            xs = wx[2 * warp];
+            xe = wx[2 * warp + 1];
+        }
+#pragma unroll
+        for (int lv = 4; lv >= 0; --lv) {
+            const int h = 1 << lv;
+            const bool left = (lane & (2 * h - 1)) == 0 && tid + h < NTh;
+            const bool right = (lane & (2 * h - 1)) == h && tid < NTh;
+            T xt = 0, xt1 = 0;
+            if (left) schur_down(sw[lv], xs, xe, xt, xt1);
+            const T r1 = __shfl_up_sync(0xffffffffu, xt1, h);
+            const T re = __shfl_up_sync(0xffffffffu, xe, h);
+            if (right) {
+                xs = r1;
+                xe = re;
+            } else if (left) {
+                xe = xt;
+            }
+        }
+        TP_GRID_STAMP(6);
+        // ---- Stage 3 of the chunks: rows from shared memory, up-sweep, back_substitute, store ----
+        auto expand = [&](int l0, int len, T cs, T ce) {
+            if (l0 < tail0 || !has_tail) {
+                Chunk<T, L> r;
+                const int64_t row0 = r0 + l0;
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    const int k = padx(l0 + i, qs);
+                    r.a[i] = sa[k];
+                    r.b[i] = sb[k];
+                    r.c[i] = sc[k];
+                    r.d[i] = sd[k];
+                }
+                T rbeta[L], gam[L], del[L], xv[L];
+                upsweep_keep<T, L>(r, rbeta, gam, del);
+                leaf_expand<T, L, L>(r, rbeta, gam, del, cs, ce, xv);
+                if (vec) store_rows<T, L, true>(x, row0, xv);
+                else store_rows<T, L, false>(x, row0, xv);
+                nf |= any_nonfinite(xv);
+                return;
+            }
+            T prev = cs;  // tail chunk: kept sweep values in shared memory
+            x[r0 + l0] = cs;
+            for (int i = 1; i < len - 1; ++i) {
+                const int k = padx(l0 + i, qs);
+                prev = (sd[k] - sa[k] * prev - sc[k] * ce) * sb[k];
+                x[r0 + l0 + i] = prev;
+                nf |= !isfinite(prev);
+            }
+            x[r0 + l0 + len - 1] = ce;
+            nf |= !isfinite(cs) || !isfinite(ce);
+        };
+        if (active) {
+            if (lb > 0) {
+                T xt, xt1;
+                schur_down(s0, xs, xe, xt, xt1);
+                expand(la0, la, xs, xt);
+                expand(lb0, lb, xt1, xe);
+            } else {
+                expand(la0, la, xs, xe);
+            }
+        }
+    }
+    TP_GRID_STAMP(7);
+    if (nf) report_nonfinite(err, r0);
+    if (mg.tripped() || flag) report_pivot(err, level, r0 + la0);
+    if (tflag) report_pivot(err, level, r0);
+}
+
 // ---------------------------------------------------------------- host side
 
 static size_t grid_smem_bytes(int64_t S, size_t elem) { return (size_t)4 * S * elem; }
@@ -1096,6 +1459,12 @@ static GregKernel<T, MODE> greg_kernel(int L) {
     return L == 8 ? k_grid_reg<T, 8, MODE> : L == 5 ? k_grid_reg<T, 5, MODE> : L == 4 ? k_grid_reg<T, 4, MODE>
            : L == 2 ? k_grid_reg<T, 2, MODE> : nullptr;
 }
+template <class T, int MODE>
+static GregKernel<T, MODE> ghyb_kernel(int L) {
+    return L == 8 ? k_grid_hyb<T, 8, MODE> : L == 5 ? k_grid_hyb<T, 5, MODE> : L == 4 ? k_grid_hyb<T, 4, MODE>
+           : L == 2 ? k_grid_hyb<T, 2, MODE> : nullptr;
+}
+static int g_ghyb = -1;  // hybrid variant (TPB_GRID_HYB=0 turns it off)
 static size_t greg_smem_bytes(size_t elem) {
     return (size_t)6 * kGridThreads * 6 * elem + (size_t)4 * kGregTail * elem;
 }
@@ -1135,6 +1504,12 @@ cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x,
             if (e == cudaSuccess && greg_kernel<T, kShard>(l) != nullptr)
                 e = cudaFuncSetAttribute(greg_kernel<T, kShard>(l), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)greg_smem_bytes(sizeof(T)));
+            if (e == cudaSuccess && ghyb_kernel<T, kSolve>(l) != nullptr)
+                e = cudaFuncSetAttribute(ghyb_kernel<T, kSolve>(l), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kGridDynSmem);
+            if (e == cudaSuccess && ghyb_kernel<T, kShard>(l) != nullptr)
+                e = cudaFuncSetAttribute(ghyb_kernel<T, kShard>(l), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kGridDynSmem);
             if (e != cudaSuccess) return e;
         }
         attr_done[sizeof(T) == 8] = true;
@@ -1159,7 +1534,22 @@ cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x,
     // 15.6 us, 1e5 {32} 10.9 vs 11.8 us, C3's level 2 17.9 vs 18.4 us;
     // tools/ab_grid_reg.sh)
     const int64_t rows_cta = ((geo.K + geo.P - 1) / geo.P) * geo.m;
-    if ((L == 8 || L == 4 || L == 2) && rows_cta <= 5000 && g_greg == 1) {
+    if (g_ghyb < 0) {
+        const char* v = getenv("TPB_GRID_HYB");
+        g_ghyb = (v != nullptr && atoi(v) == 0) ? 0 : 1;
+    }
+    // Which variant (in-graph kernel durations, tools/ab_grid_reg.sh and
+    // ab_grid_hyb.sh): 4- and 8-row chunks: k_grid_hyb (C2 19.3 vs 20.0 us,
+    // C3's level 2 16.8 vs 17.9 us, 6e5 {32} 14.3 vs 14.6 us); 2-row chunks at
+    // <= 5K rows per SM: k_grid_reg (1e5 {32} 10.9 vs 11.3 / 11.8 us); 5-row
+    // and uneven chunks: k_grid_solve (6e5 {20} 16.2 vs 18.0 us).
+    if ((L == 8 || L == 4) && g_ghyb == 1) {  // rows into registers and shared memory (k_grid_hyb)
+        auto a32 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; };
+        const int vec = a32(sys.sub) && a32(sys.diag) && a32(sys.sup) && a32(sys.rhs) && a32(x) ? 1 : 0;
+        if (mode == kShard) return cudaLaunchKernelEx(&cfg, ghyb_kernel<T, kShard>(L), sys, geo, x, pairs, bar, err, level, lk, vec);
+        return cudaLaunchKernelEx(&cfg, ghyb_kernel<T, kSolve>(L), sys, geo, x, pairs, bar, err, level, lk, vec);
+    }
+    if (L == 2 && rows_cta <= 5000 && g_greg == 1) {
         auto a32 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; };
         const int vec = a32(sys.sub) && a32(sys.diag) && a32(sys.sup) && a32(sys.rhs) && a32(x) ? 1 : 0;
         cfg.dynamicSmemBytes = greg_smem_bytes(sizeof(T));

@@ -175,10 +175,11 @@ def test_grid_observer_still_sees_the_interface(tp, oracle_mod):
 
 
 @pytest.mark.parametrize("n,m", [(100_000, 32), (400_000, 32), (600_001, 32), (262_144, 64), (50_000, 8),
-                                 (100_003, 16), (300_000, 4)])
-def test_grid_register_variant(tp, oracle_mod, n, m):
-    """k_grid_reg (rows in registers, re-read for Stage 3; L = 4 / 8 chunks, <= 5K
-    rows per SM) against the reference, tails included."""
+                                 (100_003, 16), (300_000, 4), (1_000_001, 32), (999_999, 64), (700_003, 16)])
+def test_grid_register_variants(tp, oracle_mod, n, m):
+    """k_grid_reg (2-row chunks: rows in registers, re-read from L2 for Stage 3)
+    and k_grid_hyb (4- and 8-row chunks: rows via registers into shared memory)
+    against the reference, tails included."""
     s = oracle_mod.generate_system(n, 17 + n % 7)
     ref = oracle_mod.solve_partition(s, [m], impl="port")
     x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy([m]))
