@@ -701,6 +701,24 @@ tp_status run_maybe_graph(tp_ctx* ctx, cudaStream_t st, const std::vector<int64_
     return TP_OK;
 }
 
+// A solve graph with the grid solve whose capture or launch fails (the
+// cooperative launch cannot make every CTA resident: fewer SMs available than
+// the device reports, e.g. under MPS limits) is retried once on the level
+// path, and the context keeps the level path from then on.
+template <class T, class Fn>
+tp_status run_with_grid_fallback(tp_ctx* ctx, cudaStream_t st, std::vector<int64_t> key, const Plan<T>& p, Fn&& fn,
+                                 tp_error* err) {
+    const bool grid = grid_level(ctx, p) >= 0;
+    tp_status s = run_maybe_graph<T>(ctx, st, key, fn, err);
+    if (s != TP_ERR_CUDA || !grid) return s;
+    cudaGetLastError();  // clear the launch error
+    ctx->grid_on = false;
+    drop_graphs(ctx);
+    key.push_back(-2);  // a distinct graph-cache entry for the level-path graph
+    clear_err(err);
+    return run_maybe_graph<T>(ctx, st, key, fn, err);
+}
+
 template <class T>
 std::vector<int64_t> make_key(int64_t tag, int64_t n, const int64_t* sizes, int32_t nsizes,
                               std::initializer_list<const void*> ptrs, int64_t extra = 0) {
@@ -743,7 +761,7 @@ tp_status solve_dev(tp_ctx* ctx, const T* sub, const T* diag, const T* super, co
     ctx->last.in[3] = rhs;
     ctx->last.x = x;
     auto key = make_key<T>(1, n, sizes, nsizes, {sub, diag, super, rhs, x, ctx->ws}, ctx->no_grid ? 1 : 0);
-    return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.solve(p); }, err);
+    return run_with_grid_fallback<T>(ctx, st, key, p, [&](Runner<T>& r) { r.solve(p); }, err);
 }
 
 // A solve reported a zero pivot (the device error word; dev_row / dev_level
@@ -991,7 +1009,7 @@ tp_status thomas_host(tp_ctx* ctx, const T* sub, const T* diag, const T* super, 
             for (int i = 0; i < 4; ++i) ctx->last.in[i] = d[i];
             ctx->last.x = d[4];
             auto key = make_key<T>(2, n, nullptr, 0, {d[0], d[1], d[2], d[3], d[4], ctx->ws});
-            return run_maybe_graph<T>(ctx, st, key, [&](Runner<T>& r) { r.solve(p); }, err);
+            return run_with_grid_fallback<T>(ctx, st, key, p, [&](Runner<T>& r) { r.solve(p); }, err);
         },
         err);
 }
