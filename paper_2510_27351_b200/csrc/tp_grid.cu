@@ -1477,6 +1477,9 @@ cudaError_t launch_grid_solve(const SysPtrs<T>& sys, int64_t n, int64_t m, T* x,
     GridGeom geo;
     if (!grid_geom<T>(n, m, sms, geo)) return cudaErrorInvalidValue;
     geo.flags = flags;
+    // test hook of the host's level-path fallback (TPB_GRID_FORCE_FAIL=1)
+    static const bool force_fail = [] { const char* v = getenv("TPB_GRID_FORCE_FAIL"); return v && atoi(v) != 0; }();
+    if (force_fail) return cudaErrorCooperativeLaunchTooLarge;
     if (mode == kShard && (sizeof(T) != 8 || link == nullptr || link->nranks < 1 || link->nranks > kMaxPeers))
         return cudaErrorInvalidValue;  // the mailboxes carry FP64 pairs
     unsigned* bar = static_cast<unsigned*>(scratch);

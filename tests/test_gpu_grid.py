@@ -208,3 +208,27 @@ print(json.dumps(tp.context().last_kernels()))
     assert outs["1"][1] == ["grid_solve:L0"]
     assert "grid_solve:L0" not in outs["0"][1]
     assert oracle_mod.rel_inf_diff(outs["1"][0], outs["0"][0]) <= 1e-13
+
+
+def test_grid_launch_failure_falls_back_to_the_level_path(tp, oracle_mod):
+    """A grid solve whose cooperative launch fails (TPB_GRID_FORCE_FAIL=1 makes
+    the launcher refuse, as a GPU with fewer available SMs would) is retried on
+    the level path; the context keeps the level path."""
+    code = """
+import json, sys, numpy as np
+sys.path.insert(0, %r)
+import oracle, paper_2510_27351_b200 as tp
+s = oracle.generate_system(1_000_000, 4)
+ref = oracle.solve_partition(s, [32])
+x = tp.solve_partition(tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs), tp.RecursionPolicy([32]))
+k1 = tp.context().last_kernels()
+x2 = tp.solve_partition(tp.TridiagonalSystem(s.sub, s.diag, s.sup, s.rhs), tp.RecursionPolicy([32]))
+print(json.dumps({"d": oracle.rel_inf_diff(x, ref), "d2": oracle.rel_inf_diff(x2, ref), "k1": k1,
+                  "k2": tp.context().last_kernels()}))
+""" % ROOT
+    env = dict(os.environ, TPB_GRID_FORCE_FAIL="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["d"] <= TOL and out["d2"] <= TOL
+    assert "grid_solve:L0" not in out["k1"] and "grid_solve:L0" not in out["k2"], out
