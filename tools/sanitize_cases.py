@@ -44,8 +44,11 @@ def main():
         (40_000, [64, 7]),       # fused deepest level, generic sweeps (odd m)
         (160_000, [64, 10, 8]),  # level 1 folded into level 0 (k_fast_s1fold)
         (640_000, [64, 10, 32]), # levels 1 and 2 folded (FOLD2)
-        (100_000, [32]),         # one-kernel grid solve, 8-row chunks (k_grid_solve<T, 8>)
-        (150_001, [4]),          # grid solve, 2-row chunks, tail block (k_grid_solve<T, 2>)
+        (100_000, [32]),         # one-kernel grid solve, 2-row chunks in registers (k_grid_reg<T, 2>)
+        (150_001, [4]),          # grid solve, 2-row chunks, tail block (k_grid_reg<T, 2>)
+        (600_001, [32]),         # grid solve, 4-row chunks via registers into smem, tail (k_grid_hyb<T, 4>)
+        (1_000_000, [32]),       # grid solve, 8-row chunks (k_grid_hyb<T, 8>, config 2)
+        (300_000, [20]),         # grid solve, 5-row chunks in shared memory (k_grid_solve<T, 5>)
         (90_007, [20]),          # grid solve, uneven chunks (k_grid_solve<T, 0>, loop leaves)
     ]
     worst = 0.0
