@@ -1257,6 +1257,7 @@ tp_status tp_ctx_create(int32_t device, tp_ctx** out, tp_error* err) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 64);
+    if (e == cudaSuccess) e = cudaMemset(c->d_err, 0xFF, 64);  // kNoError
     if (e == cudaSuccess) e = cudaMalloc(&c->d_red, 64);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_small, 4096);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_grid, tpb::kGridScratchBytes);

@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(kFinNT, 1)
     pdl_begin();
     TP_LF_TRACE(0);
     if ((flags & kResetErr) && cta == 0 && tid == 0 && err != nullptr) {  // the graph's only kernel
-        atomicExch(err, kNoError);
+        *reinterpret_cast<volatile unsigned long long*>(err) = kNoError;
         __threadfence();
     }
 

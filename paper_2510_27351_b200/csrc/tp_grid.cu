@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             TP_GRID_STAMP(3);
             // the graph's only kernel: reset the error word before arriving
             // (every report of this solve comes after the barrier)
-            if ((geo.flags & kResetErr) && b == 0 && err != nullptr) atomicExch(err, kNoError);
+            if ((geo.flags & kResetErr) && b == 0 && err != nullptr) *reinterpret_cast<volatile unsigned long long*>(err) = kNoError;
             __threadfence();
             atomicAdd(bar, 1u);  // arrive; the wait comes after the symbolic pass
         }
@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
             o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
             TP_GRID_STAMP(3);
-            if ((geo.flags & kResetErr) && b == 0 && err != nullptr) atomicExch(err, kNoError);
+            if ((geo.flags & kResetErr) && b == 0 && err != nullptr) *reinterpret_cast<volatile unsigned long long*>(err) = kNoError;
             __threadfence();
             atomicAdd(bar, 1u);
             long spins = 0;
@@ -1196,7 +1196,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
             o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
             TP_GRID_STAMP(3);
-            if ((geo.flags & kResetErr) && b == 0 && err != nullptr) atomicExch(err, kNoError);
+            if ((geo.flags & kResetErr) && b == 0 && err != nullptr) *reinterpret_cast<volatile unsigned long long*>(err) = kNoError;
             __threadfence();
             atomicAdd(bar, 1u);
             long spins = 0;
