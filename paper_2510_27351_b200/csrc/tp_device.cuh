@@ -344,6 +344,15 @@ __device__ __forceinline__ Eq2<T> merge_schur(const Eq2<T>& A, const Eq2<T>& B, 
     P.d2 = fma(-B.a2, sv.ud, B.d2);
     return P;
 }
+// merge_schur with RowGuard bookkeeping (the merge's row for the report).
+template <class T>
+__device__ __forceinline__ Eq2<T> merge_schur_row(const Eq2<T>& A, const Eq2<T>& B, int64_t row_t, RowGuard& bad,
+                                                  SchurSave<T>& sv) {
+    bool f = false;
+    const Eq2<T> P = merge_schur(A, B, f, sv);
+    if (f) bad.bad = row_t < bad.bad ? row_t : bad.bad;
+    return P;
+}
 template <class T>
 __device__ __forceinline__ void schur_down(const SchurSave<T>& sv, T xs, T xe, T& xt, T& xt1) {
     xt = fma(sv.sg, xe, fma(-sv.sa, xs, sv.sd));

@@ -293,13 +293,13 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
     TP_TRACE(2);
 
     // ---- warp levels (chunk index inside the CTA == tid) ----
-    MergeSave<T> sw[5];
+    SchurSave<T> sw[5];
 #pragma unroll
     for (int lv = 0; lv < 5; ++lv) {
         const int h = 1 << lv;
         const Eq2<T> oth = shfl_down_eq(cur, h);
         if (h < per && (lane & (2 * h - 1)) == 0 && tid + h < per)
-            cur = merge(cur, oth, cstart(tid + h) - 1, bad, sw[lv]);
+            cur = merge_schur_row(cur, oth, cstart(tid + h) - 1, bad, sw[lv]);
     }
     const int nwr = per >= 32 ? per / 32 : 1;
     if (lane == 0 && warp < nwr) wroot[warp] = cur;
@@ -307,7 +307,7 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
     TP_TRACE(3);
 
     // ---- warp 0: the CTA's warp roots (<= 3 levels) ----
-    MergeSave<T> sx[3];
+    SchurSave<T> sx[3];
     Eq2<T> wc = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
     if (warp == 0) {
         wc = lane < nwr ? wroot[lane] : wc;
@@ -316,7 +316,7 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
             const int h = 1 << lv;
             const Eq2<T> oth = shfl_down_eq(wc, h);
             if (h < nwr && (lane & (2 * h - 1)) == 0 && lane + h < nwr)
-                wc = merge(wc, oth, cstart(32 * (lane + h)) - 1, bad, sx[lv]);
+                wc = merge_schur_row(wc, oth, cstart(32 * (lane + h)) - 1, bad, sx[lv]);
         }
         if (lane == 0) croot = wc;
     }
@@ -329,13 +329,13 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
         Eq2<T> cc = Eq2<T>{0, 1, 0, 0, 0, 1, 0, 0};
         if (lane < CS) cc = *cl.map_shared_rank(&croot, lane);
         constexpr int kCLv = CS == 16 ? 4 : 3;  // levels over the CTA roots
-        MergeSave<T> sc3[kCLv];
+        SchurSave<T> sc3[kCLv];
 #pragma unroll
         for (int lv = 0; lv < kCLv; ++lv) {
             const int h = 1 << lv;
             const Eq2<T> oth = shfl_down_eq(cc, h);
             if ((lane & (2 * h - 1)) == 0 && lane + h < CS)
-                cc = merge(cc, oth, cta_row0(lane + h) - 1, bad, sc3[lv]);
+                cc = merge_schur_row(cc, oth, cta_row0(lane + h) - 1, bad, sc3[lv]);
         }
         T xs = 0, xe = 0;
         if (lane == 0) {
@@ -364,12 +364,12 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
 #pragma unroll
             for (int lv = kCLv - 1; lv >= 0; --lv) {
                 const int h = 1 << lv;
-                T xt = 0;
-                if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sc3[lv], xs, xe);
-                const T rxt = __shfl_up_sync(0xffffffffu, xt, h);
+                T xt = 0, xt1 = 0;
+                if ((lane & (2 * h - 1)) == 0) schur_down(sc3[lv], xs, xe, xt, xt1);
+                const T r1 = __shfl_up_sync(0xffffffffu, xt1, h);
                 const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
                 if ((lane & (2 * h - 1)) == h) {
-                    xs = first_from_e1(cc, rxt, rxe);
+                    xs = r1;
                     xe = rxe;
                 } else if ((lane & (2 * h - 1)) == 0) {
                     xe = xt;
@@ -399,12 +399,12 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
         for (int lv = 2; lv >= 0; --lv) {
             const int h = 1 << lv;
             if (h >= nwr) continue;
-            T xt = 0;
-            if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sx[lv], xs, xe);
-            const T rxt = __shfl_up_sync(0xffffffffu, xt, h);
+            T xt = 0, xt1 = 0;
+            if ((lane & (2 * h - 1)) == 0) schur_down(sx[lv], xs, xe, xt, xt1);
+            const T r1 = __shfl_up_sync(0xffffffffu, xt1, h);
             const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
             if ((lane & (2 * h - 1)) == h) {
-                xs = first_from_e1(wc, rxt, rxe);
+                xs = r1;
                 xe = rxe;
             } else if ((lane & (2 * h - 1)) == 0) {
                 xe = xt;
@@ -428,12 +428,12 @@ __device__ __forceinline__ void cl_tree(cooperative_groups::cluster_group& cl, c
     for (int lv = 4; lv >= 0; --lv) {
         const int h = 1 << lv;
         if (h >= per) continue;
-        T xt = 0;
-        if ((lane & (2 * h - 1)) == 0) xt = merge_xt(sw[lv], xs, xe);
-        const T rxt = __shfl_up_sync(0xffffffffu, xt, h);
+        T xt = 0, xt1 = 0;
+        if ((lane & (2 * h - 1)) == 0) schur_down(sw[lv], xs, xe, xt, xt1);
+        const T r1 = __shfl_up_sync(0xffffffffu, xt1, h);
         const T rxe = __shfl_up_sync(0xffffffffu, xe, h);
         if ((lane & (2 * h - 1)) == h) {
-            xs = first_from_e1(cur, rxt, rxe);
+            xs = r1;
             xe = rxe;
         } else if ((lane & (2 * h - 1)) == 0) {
             xe = xt;
