@@ -2,6 +2,8 @@
 # end-of-change measurement (round $R, default r02): bench line, reference arm,
 # launch list, ncu full captures of C3 / C2 / C1, in-graph timelines C1-C4,
 # grid-kernel phase traces. Everything lands in gpurun_out/ (copy to profiles/).
+# Under gpurun the three .ncu-rep files together exceed the 64 MiB copy-back
+# cap: run tools/round_measure_small.sh and one ncu capture per call instead.
 R=${R:-r02}
 set -x
 python bench.py > gpurun_out/${R}_bench.json 2> gpurun_out/${R}_bench.err
