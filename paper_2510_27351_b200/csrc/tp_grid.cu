@@ -1138,15 +1138,20 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             const int64_t row0 = r0 + l0;
             if (vec) load_chunk<T, L, true>(sys, row0, true, r);
             else load_chunk<T, L, false>(sys, row0, true, r);
+            // sweep with the up-sweep's values kept (rcp(beta_i), gamma_i,
+            // delta_i) and store those with a_i: Stage 3 then only
+            // back-substitutes (no second sweep)
+            T rbeta[L] = {}, gam[L] = {}, del[L] = {};
+            const Eq2<T> e = leaf_reduce_keep<T, L, L>(r, row0, mg, rbeta, gam, del);
 #pragma unroll
             for (int i = 0; i < L; ++i) {
                 const int k = padx(l0 + i, qs);
                 sa[k] = r.a[i];
-                sb[k] = r.b[i];
-                sc[k] = r.c[i];
-                sd[k] = r.d[i];
+                sb[k] = rbeta[i];
+                sc[k] = gam[i];
+                sd[k] = del[i];
             }
-            return leaf_reduce<T, L, L>(r, row0, mg);
+            return e;
         }
         Eq2<T> e;
         leaf_loop<T>(sa, sb, sc, sd, l0, len, qs, flag, e);
@@ -1365,16 +1370,15 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             if (l0 < tail0 || !has_tail) {
                 Chunk<T, L> r;
                 const int64_t row0 = r0 + l0;
+                T rbeta[L], gam[L], del[L], xv[L];
 #pragma unroll
                 for (int i = 0; i < L; ++i) {
                     const int k = padx(l0 + i, qs);
                     r.a[i] = sa[k];
-                    r.b[i] = sb[k];
-                    r.c[i] = sc[k];
-                    r.d[i] = sd[k];
+                    rbeta[i] = sb[k];
+                    gam[i] = sc[k];
+                    del[i] = sd[k];
                 }
-                T rbeta[L], gam[L], del[L], xv[L];
-                upsweep_keep<T, L>(r, rbeta, gam, del);
                 leaf_expand<T, L, L>(r, rbeta, gam, del, cs, ce, xv);
                 if (vec) store_rows<T, L, true>(x, row0, xv);
                 else store_rows<T, L, false>(x, row0, xv);
