@@ -232,3 +232,23 @@ print(json.dumps({"d": oracle.rel_inf_diff(x, ref), "d2": oracle.rel_inf_diff(x2
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["d"] <= TOL and out["d2"] <= TOL
     assert "grid_solve:L0" not in out["k1"] and "grid_solve:L0" not in out["k2"], out
+
+
+def test_grid_at_deeper_levels_random(tp, oracle_mod):
+    """Random multi-level policies at sizes where the grid solve takes a level
+    k >= 1 (Stage 1 above it, Stage 3 below): FP64 at the parity gates, FP32
+    against the reference's float instantiation's tolerance (1e-4)."""
+    rng = np.random.default_rng(4242)
+    for case in range(16):
+        n = int(np.exp(rng.uniform(np.log(3e5), np.log(6e6))))
+        depth = int(rng.integers(1, 4))
+        sizes = [int(rng.choice([4, 8, 10, 16, 20, 32, 64]))] + \
+                [int(rng.choice([2, 4, 8, 10, 16, 32])) for _ in range(depth)]
+        s = oracle_mod.generate_system(n, 700 + case)
+        ref = oracle_mod.solve_partition(s, sizes, impl="port")
+        x = tp.solve_partition(_sys(tp, s), tp.RecursionPolicy(sizes))
+        _check(oracle_mod, s, x, ref)
+        if case % 4 == 0:
+            args = [a.astype(np.float32) for a in (s.sub, s.diag, s.sup, s.rhs)]
+            x32 = tp.solve_partition(tp.TridiagonalSystem(*args), tp.RecursionPolicy(sizes))
+            assert oracle_mod.rel_inf_diff(x32.astype(np.float64), ref) <= 1e-4, (n, sizes)
