@@ -306,6 +306,8 @@ constexpr int kGridWarps = kGridThreads / 32;
 constexpr int kGridChunksPerThread = 2;
 // grid-barrier spin bound (>= 32 ns each): ~0.5-1 s before the solve reports an error
 constexpr long kGridSpins = 1L << 24;
+// the same bound for a tight spin (each poll an L2 round trip, ~0.3-0.5 us): ~1-2 s
+constexpr long kGridSpinsTight = 1L << 22;
 // phase timestamps (%globaltimer) of every CTA when a launch asks for them
 constexpr int kGridTraceSlots = 16;  // per CTA
 __device__ unsigned long long g_grid_trace[2 * 256 * kGridTraceSlots];  // [0, 4096) %globaltimer, then clock64
@@ -1139,17 +1141,19 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             if (vec) load_chunk<T, L, true>(sys, row0, true, r);
             else load_chunk<T, L, false>(sys, row0, true, r);
             // sweep with the up-sweep's values kept (rcp(beta_i), gamma_i,
-            // delta_i) and store those with a_i: Stage 3 then only
-            // back-substitutes (no second sweep)
+            // delta_i); back_substitute (partition.hpp:163-170) of interior
+            // row i is x_i = (delta_i - a_i x_{i-1} - gamma_i x_e) / beta_i =
+            // p_i - q_i x_{i-1} - r_i x_e, so the interior rows keep
+            // p = delta/beta, q = a/beta, r = gamma/beta (3 shared-memory
+            // values per row, and one dependent FMA per row in Stage 3)
             T rbeta[L] = {}, gam[L] = {}, del[L] = {};
             const Eq2<T> e = leaf_reduce_keep<T, L, L>(r, row0, mg, rbeta, gam, del);
 #pragma unroll
-            for (int i = 0; i < L; ++i) {
+            for (int i = 1; i < L - 1; ++i) {
                 const int k = padx(l0 + i, qs);
-                sa[k] = r.a[i];
-                sb[k] = rbeta[i];
-                sc[k] = gam[i];
-                sd[k] = del[i];
+                sa[k] = r.a[i] * rbeta[i];
+                sb[k] = del[i] * rbeta[i];
+                sc[k] = gam[i] * rbeta[i];
             }
             return e;
         }
@@ -1171,7 +1175,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     TP_GRID_STAMP(2);
 
     // ---- thread tree (5 shuffle levels), saves in registers ----
-    SchurSave<T> sw[5];
+    SchurSave<T> sw[5] = {};  // read (unused) by the non-merging lanes going down
 #pragma unroll
     for (int lv = 0; lv < 5; ++lv) {
         const int h = 1 << lv;
@@ -1202,18 +1206,21 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
             TP_GRID_STAMP(3);
             if ((geo.flags & kResetErr) && b == 0 && err != nullptr) *reinterpret_cast<volatile unsigned long long*>(err) = kNoError;
+            // tight spin (a __nanosleep between polls measured 0.4-0.5 us
+            // slower at C2; a release-add with relaxed polls slower still)
             __threadfence();
             atomicAdd(bar, 1u);
             long spins = 0;
             while (ld_acquire_gpu(bar) < (unsigned)P) {
-                if (++spins > kGridSpins) {
+                if (++spins > kGridSpinsTight) {
                     if (err != nullptr)
                         atomicMin(err, ((unsigned long long)kGridBarrierLevel << 48) | (unsigned long long)b);
                     break;
                 }
-                __nanosleep(32);
             }
-            if constexpr (MODE != kShard) grid_depart(bar, P);
+            // no departure here: its atomic returns a value, and the wait for
+            // it would hold the CTA's next __syncthreads (an idle warp departs
+            // during the top tree instead)
             TP_GRID_STAMP(9);
         }
     }
@@ -1230,13 +1237,22 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 tc = Eq2<T>{__ldcg(q + 0), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3),
                             __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
             }
-#pragma unroll
+            if (tr && tc.b1 != T(-1.2345e-300)) TP_GRID_STAMP(10);
+            // rolled: one copy of the level's code, fetched once into the
+            // instruction cache (this phase runs once per launch, cold)
+#pragma unroll 1
             for (int lv = 0; lv < 5; ++lv) {
                 const int h = 1 << lv;
                 const Eq2<T> oth = shfl_down_eq(tc, h);
+                // every lane merges (straight-line code: the serial phases after
+                // the grid barrier run from a cold instruction cache, where each
+                // divergent branch costs a fetch round trip); the tree's lanes keep it
+                SchurSave<T> sv;
+                bool f = false;
+                const Eq2<T> pm = merge_schur(tc, oth, f, sv);
                 if ((lane & (2 * h - 1)) == 0 && tid + h < P) {
-                    SchurSave<T> sv;
-                    tc = merge_schur(tc, oth, tflag, sv);
+                    tc = pm;
+                    tflag |= f;
                     if ((tid >> (lv + 1)) == (b >> (lv + 1))) {
                         tpath[3 + lv] = sv;
                         tside[3 + lv] = ((b >> lv) & 1) ? 2 : 1;
@@ -1244,18 +1260,24 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 }
             }
             if (lane == 0) troot[warp] = tc;
+            TP_GRID_STAMP(11);
         }
+        if constexpr (MODE != kShard)
+            if (tid == kGridThreads - 32) grid_depart(bar, P);  // warp 15: never a top-tree warp (P <= 256)
         __syncthreads();
         if (warp == 0) {
             Eq2<T> rc = lane < ntw ? troot[lane] : identity_eq<T>();
             const int bw = b >> 5;
-#pragma unroll
+#pragma unroll 1
             for (int lv = 0; lv < 3; ++lv) {
                 const int h = 1 << lv;
                 const Eq2<T> oth = shfl_down_eq(rc, h);
+                SchurSave<T> sv;
+                bool f = false;
+                const Eq2<T> pm = merge_schur(rc, oth, f, sv);
                 if ((lane & (2 * h - 1)) == 0 && lane + h < ntw) {
-                    SchurSave<T> sv;
-                    rc = merge_schur(rc, oth, tflag, sv);
+                    rc = pm;
+                    tflag |= f;
                     if ((lane >> (lv + 1)) == (bw >> (lv + 1))) {
                         tpath[2 - lv] = sv;
                         tside[2 - lv] = ((bw >> lv) & 1) ? 2 : 1;
@@ -1263,6 +1285,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 }
             }
             __syncwarp();
+            TP_GRID_STAMP(12);
             if (lane == 0) {
                 T xs = 0, xe = 0;
                 if constexpr (MODE == kShard) {
@@ -1308,6 +1331,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 }
                 cx[0] = xs;
                 cx[1] = xe;
+                TP_GRID_STAMP(13);
             }
         }
         __syncthreads();
@@ -1324,8 +1348,8 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             for (int j = 0; j < lv; ++j) off += kGridWarps >> (j + 1);
             const bool left = (lane & (2 * h - 1)) == 0 && lane + h < nwr;
             const bool right = (lane & (2 * h - 1)) == h && lane < nwr;
-            T xt = 0, xt1 = 0;
-            if (left) schur_down(wsv[off + (lane >> (lv + 1))], xs, xe, xt, xt1);
+            T xt, xt1;
+            schur_down(wsv[left ? off + (lane >> (lv + 1)) : 0], xs, xe, xt, xt1);
             const T r1 = __shfl_up_sync(0xffffffffu, xt1, h);
             const T re = __shfl_up_sync(0xffffffffu, xe, h);
             if (right) {
@@ -1339,8 +1363,10 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             wx[2 * lane] = xs;
             wx[2 * lane + 1] = xe;
         }
+        TP_GRID_STAMP(4);
     }
     __syncthreads();
+    TP_GRID_STAMP(14);
     bool nf = false;
     {
         T xs = 0, xe = 0;
@@ -1353,8 +1379,8 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             const int h = 1 << lv;
             const bool left = (lane & (2 * h - 1)) == 0 && tid + h < NTh;
             const bool right = (lane & (2 * h - 1)) == h && tid < NTh;
-            T xt = 0, xt1 = 0;
-            if (left) schur_down(sw[lv], xs, xe, xt, xt1);
+            T xt, xt1;
+            schur_down(sw[lv], xs, xe, xt, xt1);
             const T r1 = __shfl_up_sync(0xffffffffu, xt1, h);
             const T re = __shfl_up_sync(0xffffffffu, xe, h);
             if (right) {
@@ -1368,18 +1394,24 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         // ---- Stage 3 of the chunks: rows from shared memory, up-sweep, back_substitute, store ----
         auto expand = [&](int l0, int len, T cs, T ce) {
             if (l0 < tail0 || !has_tail) {
-                Chunk<T, L> r;
                 const int64_t row0 = r0 + l0;
-                T rbeta[L], gam[L], del[L], xv[L];
+                T q[L], pv[L], rv[L], xv[L];
 #pragma unroll
-                for (int i = 0; i < L; ++i) {
+                for (int i = 1; i < L - 1; ++i) {
                     const int k = padx(l0 + i, qs);
-                    r.a[i] = sa[k];
-                    rbeta[i] = sb[k];
-                    gam[i] = sc[k];
-                    del[i] = sd[k];
+                    q[i] = sa[k];
+                    pv[i] = sb[k];
+                    rv[i] = sc[k];
                 }
-                leaf_expand<T, L, L>(r, rbeta, gam, del, cs, ce, xv);
+                if (tr && q[1] != T(-1.2345e-300)) TP_GRID_STAMP(15);
+                xv[0] = cs;
+                T prev = cs;
+#pragma unroll
+                for (int i = 1; i < L - 1; ++i) {
+                    prev = fma(-q[i], prev, fma(-rv[i], ce, pv[i]));
+                    xv[i] = prev;
+                }
+                xv[L - 1] = ce;
                 if (vec) store_rows<T, L, true>(x, row0, xv);
                 else store_rows<T, L, false>(x, row0, xv);
                 nf |= any_nonfinite(xv);
@@ -1397,14 +1429,13 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             nf |= !isfinite(cs) || !isfinite(ce);
         };
         if (active) {
-            if (lb > 0) {
-                T xt, xt1;
-                schur_down(s0, xs, xe, xt, xt1);
-                expand(la0, la, xs, xt);
-                expand(lb0, lb, xt1, xe);
-            } else {
-                expand(la0, la, xs, xe);
-            }
+            // the two chunks through ONE copy of the expand code (its second
+            // pass runs from a warm instruction cache)
+            T xt = xe, xt1 = T(0);
+            if (lb > 0) schur_down(s0, xs, xe, xt, xt1);
+            const int nch = lb > 0 ? 2 : 1;
+#pragma unroll 1
+            for (int c = 0; c < nch; ++c) expand(c ? lb0 : la0, c ? lb : la, c ? xt1 : xs, c ? xe : xt);
         }
     }
     TP_GRID_STAMP(7);

@@ -13,10 +13,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 SLOTS = 16
-# slot -> phase name, in time order
+# slot -> phase name (printed in median-time order; a kernel stamps a subset)
 PHASES = [(0, "start"), (1, "staged"), (2, "leaves"), (8, "thread tree"), (3, "pair published"),
-          (4, "symbolic done"), (9, "barrier passed"), (10, "pairs loaded"), (11, "top warp tree"),
-          (12, "top root tree"), (13, "root + path"), (5, "top synced"), (6, "x stored"), (7, "end")]
+          (4, "symbolic done | warp-root down"), (9, "barrier passed"), (10, "pairs loaded"), (11, "top warp tree"),
+          (12, "top root tree"), (13, "root + path"), (5, "top synced"), (14, "CTA down start"),
+          (6, "x stored / thread down"), (15, "expand rows in"), (7, "end")]
 
 
 def main():
@@ -54,7 +55,9 @@ def main():
     t0 = t[:, 0].min()
     d = (t - t0) / 1000.0
     rows = {}
-    for k, ph in PHASES:
+    used = [(k, ph) for k, ph in PHASES if np.all(allv[0][live][:, k] > 0)]
+    used.sort(key=lambda kp: float(np.median(d[:, kp[0]])))
+    for k, ph in used:
         rows[ph] = [round(float(np.min(d[:, k])), 3), round(float(np.median(d[:, k])), 3),
                     round(float(np.max(d[:, k])), 3)]
         print(f"{ph:>9}  min {rows[ph][0]:8.3f}  med {rows[ph][1]:8.3f}  max {rows[ph][2]:8.3f} us"
