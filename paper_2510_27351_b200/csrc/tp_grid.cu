@@ -311,6 +311,9 @@ constexpr long kGridSpinsTight = 1L << 22;
 // phase timestamps (%globaltimer) of every CTA when a launch asks for them
 constexpr int kGridTraceSlots = 16;  // per CTA
 __device__ unsigned long long g_grid_trace[2 * 256 * kGridTraceSlots];  // [0, 4096) %globaltimer, then clock64
+// (trace builds only: `make TRACE=1`; the stamps' predicated stores and their
+// value tests cost ~0.5 us of the C2 solve's serial phases)
+#ifdef TPB_GRID_TRACE_BUILD
 #define TP_GRID_STAMP(k)                                                                           \
     do {                                                                                           \
         if (tr) {                                                                                  \
@@ -318,6 +321,12 @@ __device__ unsigned long long g_grid_trace[2 * 256 * kGridTraceSlots];  // [0, 4
             g_grid_trace[256 * kGridTraceSlots + kGridTraceSlots * b + (k)] = clock64();           \
         }                                                                                          \
     } while (0)
+#else
+#define TP_GRID_STAMP(k) \
+    do {                 \
+        (void)tr;        \
+    } while (0)
+#endif
 
 // Block range of CTA b: blocks [K*b/P, K*(b+1)/P) of make_plan(n, m).
 struct GridGeom {
@@ -1238,15 +1247,14 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                             __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
             }
             if (tr && tc.b1 != T(-1.2345e-300)) TP_GRID_STAMP(10);
-            // rolled: one copy of the level's code, fetched once into the
-            // instruction cache (this phase runs once per launch, cold)
+            // rolled: one copy of the level's code (this phase runs once per
+            // launch; a dry pass by an idle warp to warm the instruction
+            // cache, through a non-inlined copy, measured 0.7 us slower)
 #pragma unroll 1
             for (int lv = 0; lv < 5; ++lv) {
                 const int h = 1 << lv;
                 const Eq2<T> oth = shfl_down_eq(tc, h);
-                // every lane merges (straight-line code: the serial phases after
-                // the grid barrier run from a cold instruction cache, where each
-                // divergent branch costs a fetch round trip); the tree's lanes keep it
+                // every lane merges (straight-line code); the tree's lanes keep it
                 SchurSave<T> sv;
                 bool f = false;
                 const Eq2<T> pm = merge_schur(tc, oth, f, sv);

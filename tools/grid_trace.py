@@ -1,7 +1,11 @@
 """Phase timeline of one k_grid_solve launch (TPB_GRID_TRACE=1): per phase, the
 min / median / max over CTAs of %globaltimer offsets from the earliest CTA start.
 
-    TPB_GRID_TRACE=1 python tools/grid_trace.py --n 1e6 --policy 32
+    make -C paper_2510_27351_b200/csrc TRACE=1 OUT=../lib/trace
+    TPB_LIB=paper_2510_27351_b200/lib/trace/libtridpart_b200.so TPB_GRID_TRACE=1 \
+        python tools/grid_trace.py --n 1e6 --policy 32
+
+(the stamps are compiled only into trace builds; the default library has none)
 """
 import argparse
 import ctypes as C
