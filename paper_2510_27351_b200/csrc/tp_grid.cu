@@ -350,6 +350,32 @@ __device__ __forceinline__ void grid_depart(unsigned* bar, int P) {
     }
 }
 
+// A CTA pair in its 64-byte slot: two 256-bit stores / L2 loads (every CTA
+// reads all P slots right after the grid barrier; 4x fewer requests on those
+// hot L2 lines than 8-byte accesses). FP32: 8 scalar accesses.
+__device__ __forceinline__ void store_cta_pair(double* o, const Eq2<double>& q) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o), "d"(q.a1), "d"(q.b1), "d"(q.g1), "d"(q.d1)
+                 : "memory");
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o + 4), "d"(q.a2), "d"(q.b2), "d"(q.g2), "d"(q.d2)
+                 : "memory");
+}
+__device__ __forceinline__ Eq2<double> load_cta_pair(const double* q) {
+    Eq2<double> r;
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.a1), "=d"(r.b1), "=d"(r.g1), "=d"(r.d1) : "l"(q) : "memory");
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.a2), "=d"(r.b2), "=d"(r.g2), "=d"(r.d2) : "l"(q + 4) : "memory");
+    return r;
+}
+__device__ __forceinline__ void store_cta_pair(float* o, const Eq2<float>& q) {
+    o[0] = q.a1; o[1] = q.b1; o[2] = q.g1; o[3] = q.d1;
+    o[4] = q.a2; o[5] = q.b2; o[6] = q.g2; o[7] = q.d2;
+}
+__device__ __forceinline__ Eq2<float> load_cta_pair(const float* q) {
+    return Eq2<float>{__ldcg(q + 0), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3),
+                      __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
+}
+
 // MODE kSolve: the root pair is the whole system (thomas_solve on [E1; E2]).
 // MODE kShard: the root pair is this rank's shard; CTA 0 exchanges it with
 // every peer over peer memory (shard_exchange, tp_exchange.cuh), solves the
@@ -475,9 +501,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             }
         }
         if (lane == 0) {
-            T* o = pairs + 8 * (int64_t)b;
-            o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
-            o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
+            store_cta_pair(pairs + 8 * (int64_t)b, wc);
             TP_GRID_STAMP(3);
             // the graph's only kernel: reset the error word before arriving
             // (every report of this solve comes after the barrier)
@@ -535,20 +559,16 @@ __global__ void __launch_bounds__(kGridThreads, 1)
 
     // ---- the grid barrier: every CTA's pair is published ----
     if (tid == 0) {
-        long spins = 0;
+        long spins = 0;  // tight spin; departure on warp 15 (as k_grid_hyb)
         while (ld_acquire_gpu(bar) < (unsigned)P) {
-            if (++spins > kGridSpins) {
+            if (++spins > kGridSpinsTight) {
                 if (err != nullptr)
                     atomicMin(err, ((unsigned long long)kGridBarrierLevel << 48) | (unsigned long long)b);
                 break;
             }
-            __nanosleep(32);
         }
     }
     TP_GRID_STAMP(9);
-    if constexpr (MODE != kShard) {
-        if (tid == 0) grid_depart(bar, P);
-    }
     __syncthreads();
 
     // ---- every CTA: the tree over the P CTA pairs (identical arithmetic in
@@ -558,11 +578,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         const int ntw = (P + 31) / 32;
         if (warp < ntw) {
             Eq2<T> tc = identity_eq<T>();
-            if (tid < P) {
-                const T* q = pairs + 8 * (int64_t)tid;
-                tc = Eq2<T>{__ldcg(q + 0), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3),
-                            __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
-            }
+            if (tid < P) tc = load_cta_pair(pairs + 8 * (int64_t)tid);
             if (tr) { volatile T sink = tc.d2; (void)sink; }
             TP_GRID_STAMP(10);
 #pragma unroll
@@ -581,6 +597,8 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             if (lane == 0) troot[warp] = tc;
             TP_GRID_STAMP(11);
         }
+        if constexpr (MODE != kShard)
+            if (tid == kGridThreads - 32) grid_depart(bar, P);  // warp 15: never a top-tree warp (P <= 256)
         __syncthreads();
         if (warp == 0) {
             Eq2<T> rc = lane < ntw ? troot[lane] : identity_eq<T>();
@@ -845,23 +863,19 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             }
         }
         if (lane == 0) {
-            T* o = pairs + 8 * (int64_t)b;
-            o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
-            o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
+            store_cta_pair(pairs + 8 * (int64_t)b, wc);
             TP_GRID_STAMP(3);
             if ((geo.flags & kResetErr) && b == 0 && err != nullptr) *reinterpret_cast<volatile unsigned long long*>(err) = kNoError;
             __threadfence();
             atomicAdd(bar, 1u);
-            long spins = 0;
+            long spins = 0;  // tight spin; departure on warp 15 (as k_grid_hyb)
             while (ld_acquire_gpu(bar) < (unsigned)P) {
-                if (++spins > kGridSpins) {
+                if (++spins > kGridSpinsTight) {
                     if (err != nullptr)
                         atomicMin(err, ((unsigned long long)kGridBarrierLevel << 48) | (unsigned long long)b);
                     break;
                 }
-                __nanosleep(32);
             }
-            if constexpr (MODE != kShard) grid_depart(bar, P);
             TP_GRID_STAMP(9);
         }
     }
@@ -873,11 +887,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         const int ntw = (P + 31) / 32;
         if (warp < ntw) {
             Eq2<T> tc = identity_eq<T>();
-            if (tid < P) {
-                const T* q = pairs + 8 * (int64_t)tid;
-                tc = Eq2<T>{__ldcg(q + 0), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3),
-                            __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
-            }
+            if (tid < P) tc = load_cta_pair(pairs + 8 * (int64_t)tid);
 #pragma unroll
             for (int lv = 0; lv < 5; ++lv) {
                 const int h = 1 << lv;
@@ -893,6 +903,8 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             }
             if (lane == 0) troot[warp] = tc;
         }
+        if constexpr (MODE != kShard)
+            if (tid == kGridThreads - 32) grid_depart(bar, P);  // warp 15: never a top-tree warp (P <= 256)
         __syncthreads();
         if (warp == 0) {
             Eq2<T> rc = lane < ntw ? troot[lane] : identity_eq<T>();
@@ -1210,9 +1222,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
             }
         }
         if (lane == 0) {
-            T* o = pairs + 8 * (int64_t)b;
-            o[0] = wc.a1; o[1] = wc.b1; o[2] = wc.g1; o[3] = wc.d1;
-            o[4] = wc.a2; o[5] = wc.b2; o[6] = wc.g2; o[7] = wc.d2;
+            store_cta_pair(pairs + 8 * (int64_t)b, wc);
             TP_GRID_STAMP(3);
             if ((geo.flags & kResetErr) && b == 0 && err != nullptr) *reinterpret_cast<volatile unsigned long long*>(err) = kNoError;
             // tight spin (a __nanosleep between polls measured 0.4-0.5 us
@@ -1241,11 +1251,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         const int ntw = (P + 31) / 32;
         if (warp < ntw) {
             Eq2<T> tc = identity_eq<T>();
-            if (tid < P) {
-                const T* q = pairs + 8 * (int64_t)tid;
-                tc = Eq2<T>{__ldcg(q + 0), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3),
-                            __ldcg(q + 4), __ldcg(q + 5), __ldcg(q + 6), __ldcg(q + 7)};
-            }
+            if (tid < P) tc = load_cta_pair(pairs + 8 * (int64_t)tid);
             if (tr && tc.b1 != T(-1.2345e-300)) TP_GRID_STAMP(10);
             // rolled: one copy of the level's code (this phase runs once per
             // launch; a dry pass by an idle warp to warm the instruction
