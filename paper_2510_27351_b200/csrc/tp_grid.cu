@@ -41,6 +41,14 @@ namespace tpb {
 
 namespace {
 
+// A copy of v the compiler cannot rematerialise: keeps loop-carried indices
+// (tid, blockIdx) in registers instead of re-reading them with S2R, whose
+// latency sat on the serial tree loops' critical path.
+__device__ __forceinline__ int pin_reg(int v) {
+    int r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -1250,8 +1258,9 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     {
         const int ntw = (P + 31) / 32;
         if (warp < ntw) {
+            const int ptid = pin_reg(tid), pb = pin_reg(b);
             Eq2<T> tc = identity_eq<T>();
-            if (tid < P) tc = load_cta_pair(pairs + 8 * (int64_t)tid);
+            if (ptid < P) tc = load_cta_pair(pairs + 8 * (int64_t)ptid);
             if (tr && tc.b1 != T(-1.2345e-300)) TP_GRID_STAMP(10);
             // rolled: one copy of the level's code (this phase runs once per
             // launch; a dry pass by an idle warp to warm the instruction
@@ -1264,12 +1273,12 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 SchurSave<T> sv;
                 bool f = false;
                 const Eq2<T> pm = merge_schur(tc, oth, f, sv);
-                if ((lane & (2 * h - 1)) == 0 && tid + h < P) {
+                if ((ptid & (2 * h - 1)) == 0 && ptid + h < P) {
                     tc = pm;
                     tflag |= f;
-                    if ((tid >> (lv + 1)) == (b >> (lv + 1))) {
+                    if ((ptid >> (lv + 1)) == (pb >> (lv + 1))) {
                         tpath[3 + lv] = sv;
-                        tside[3 + lv] = ((b >> lv) & 1) ? 2 : 1;
+                        tside[3 + lv] = ((pb >> lv) & 1) ? 2 : 1;
                     }
                 }
             }
@@ -1281,7 +1290,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         __syncthreads();
         if (warp == 0) {
             Eq2<T> rc = lane < ntw ? troot[lane] : identity_eq<T>();
-            const int bw = b >> 5;
+            const int bw = pin_reg(b >> 5), plane = pin_reg(lane);
 #pragma unroll 1
             for (int lv = 0; lv < 3; ++lv) {
                 const int h = 1 << lv;
@@ -1289,10 +1298,10 @@ __global__ void __launch_bounds__(kGridThreads, 1)
                 SchurSave<T> sv;
                 bool f = false;
                 const Eq2<T> pm = merge_schur(rc, oth, f, sv);
-                if ((lane & (2 * h - 1)) == 0 && lane + h < ntw) {
+                if ((plane & (2 * h - 1)) == 0 && plane + h < ntw) {
                     rc = pm;
                     tflag |= f;
-                    if ((lane >> (lv + 1)) == (bw >> (lv + 1))) {
+                    if ((plane >> (lv + 1)) == (bw >> (lv + 1))) {
                         tpath[2 - lv] = sv;
                         tside[2 - lv] = ((bw >> lv) & 1) ? 2 : 1;
                     }
