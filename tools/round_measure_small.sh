@@ -9,4 +9,4 @@ python tools/timeline.py --out gpurun_out/${R}_timeline_c3.json > gpurun_out/${R
 python tools/timeline.py --n 1e6 --policy 32 --out gpurun_out/${R}_timeline_c2.json > gpurun_out/${R}_timeline_c2.txt 2>&1
 python tools/timeline.py --n 1e9 --policy 64,10,32,32 --out gpurun_out/${R}_timeline_c4.json > gpurun_out/${R}_timeline_c4.txt 2>&1
 python tools/timeline.py --n 1e4 --policy 4 --out gpurun_out/${R}_timeline_c1.json > gpurun_out/${R}_timeline_c1.txt 2>&1
-TPB_GRID_TRACE=1 python tools/grid_trace.py --n 1e6 --policy 32 --out gpurun_out/${R}_grid_trace_c2.json > gpurun_out/${R}_grid_trace_c2.txt 2>&1
+TPB_LIB=paper_2510_27351_b200/lib/trace/libtridpart_b200.so TPB_GRID_TRACE=1 python tools/grid_trace.py --n 1e6 --policy 32 --out gpurun_out/${R}_grid_trace_c2.json > gpurun_out/${R}_grid_trace_c2.txt 2>&1
