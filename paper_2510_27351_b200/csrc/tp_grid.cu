@@ -345,7 +345,14 @@ struct GridGeom {
     int qs;  // pad shift (one pad element per 2^qs rows)
     int trace;
     int flags;  // kResetErr: the graph's only kernel resets the error word
+    int64_t kq;  // K / P and K % P: CTA b's first block K*b/P = kq*b + (kr*b)/P
+    int kr;      // with one 32-bit division (kr*b < 2^16), not a 64-bit one
 };
+
+// First plan block of CTA b (b = P gives K): floor(K * b / P).
+__device__ __forceinline__ int64_t cta_block0(const GridGeom& g, int b) {
+    return g.kq * b + (int64_t)((unsigned)(g.kr * b) / (unsigned)g.P);
+}
 
 // The grid barrier's counters: bar[0] counts arrivals (P, then P + 1 when
 // the sharded root ends are out), bar[1] departures. The last CTA to leave
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     TP_GRID_STAMP(0);
 
     // ---- this CTA's rows: whole blocks [kb0, kb1) ----
-    const int64_t kb0 = K * b / P, kb1 = K * (b + 1) / P;
+    const int64_t kb0 = cta_block0(geo, b), kb1 = cta_block0(geo, b + 1);
     const int64_t r0 = kb0 * m;
     const int64_t r1 = (kb1 == K) ? n : kb1 * m;
     const int R = (int)(r1 - r0);
@@ -768,7 +775,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     TP_GRID_STAMP(0);
 
     // ---- this CTA's rows: whole blocks [kb0, kb1) (as k_grid_solve) ----
-    const int64_t kb0 = K * b / P, kb1 = K * (b + 1) / P;
+    const int64_t kb0 = cta_block0(geo, b), kb1 = cta_block0(geo, b + 1);
     const int64_t r0 = kb0 * m;
     const int64_t r1 = (kb1 == K) ? n : kb1 * m;
     const int R = (int)(r1 - r0);
@@ -1112,7 +1119,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     TP_GRID_STAMP(0);
 
     // ---- this CTA's rows: whole blocks [kb0, kb1) (as k_grid_solve) ----
-    const int64_t kb0 = K * b / P, kb1 = K * (b + 1) / P;
+    const int64_t kb0 = cta_block0(geo, b), kb1 = cta_block0(geo, b + 1);
     const int64_t r0 = kb0 * m;
     const int64_t r1 = (kb1 == K) ? n : kb1 * m;
     const int R = (int)(r1 - r0);
@@ -1493,7 +1500,7 @@ static bool grid_geom(int64_t n, int64_t m, int sms, GridGeom& geo) {
     const int64_t S = ((rows + (rows >> qs) + 1 + 3) / 4) * 4;
     if (grid_smem_bytes(S, sizeof(T)) > kGridDynSmem) return false;
     static const int trace = [] { const char* v = getenv("TPB_GRID_TRACE"); return v ? atoi(v) : 0; }();
-    geo = GridGeom{n, m, K, lg, P, (int)S, qs, trace, 0};
+    geo = GridGeom{n, m, K, lg, P, (int)S, qs, trace, 0, K / P, (int)(K % P)};
     return true;
 }
 
