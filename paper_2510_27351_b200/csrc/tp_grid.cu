@@ -6,8 +6,9 @@
 // (1e6 rows -> a 62,500-row interface), the finishing solve of that interface
 // on ONE 16-CTA cluster (16 of 148 SMs, 10.5 us of a 23 us solve), Stage 3.
 // Here every SM owns a contiguous run of whole level-0 blocks
-// (make_plan, partition.hpp:30-49), stages it in shared memory ONCE with TMA
-// bulk copies, and the rest never leaves the chip:
+// (make_plan, partition.hpp:30-49), stages it in shared memory ONCE
+// (per-element cp.async into a padded layout; k_grid_hyb: 256-bit register
+// loads), and the rest never leaves the chip:
 //   leaf sweeps of each chunk (reduce_block's up-/down-sweep, partition.hpp:
 //   90-124, intermediate values kept in place for back_substitute :156-172)
 //   -> chunk tree (shuffles, then warp roots) to the CTA's pair E1/E2
@@ -1086,10 +1087,11 @@ __global__ void __launch_bounds__(kGridThreads, 1)
 
 // ===========================================================================
 // k_grid_hyb: rows loaded into registers (256-bit) and swept from there, as
-// k_grid_reg, but also copied into the padded shared-memory layout of
-// k_grid_solve, so Stage 3 reads them back from shared memory instead of L2;
-// the merge saves stay in registers (as k_grid_solve). Shared-memory traffic:
-// 8 values per row (k_grid_solve: 17), no L2 re-read (k_grid_reg).
+// k_grid_reg; each interior row keeps p = delta/beta, q = a/beta, r =
+// gamma/beta in the padded shared-memory layout of k_grid_solve, so Stage 3 is
+// one FMA chain per chunk from shared memory instead of an L2 re-read; the
+// merge saves stay in registers (as k_grid_solve). Shared-memory traffic: 6
+// values per interior row (k_grid_solve: 17), no L2 re-read (k_grid_reg).
 // ===========================================================================
 template <class T, int L, int MODE>
 __global__ void __launch_bounds__(kGridThreads, 1)
